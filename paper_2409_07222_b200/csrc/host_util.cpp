@@ -1,0 +1,211 @@
+// host_util.cpp -- see host_util.hpp.
+#include "host_util.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+namespace labs_b200 {
+
+uint64_t splitmix64(uint64_t& s) {
+    s += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+const TabTables& TabTables::get() {
+    static const TabTables* inst = [] {
+        auto* tt = new TabTables();
+        uint64_t sm = 0x5eed5eed5eed5eedULL;
+        for (auto& table : tt->t)
+            for (auto& pos : table)
+                for (auto& v : pos) v = splitmix64(sm);
+        for (auto& table : tt->salt)
+            for (auto& v : table) v = splitmix64(sm);
+        return tt;
+    }();
+    return *inst;
+}
+
+uint64_t TabTables::hash(const int8_t* s, int n, int table) const {
+    uint64_t h = salt[table][n];
+    for (int i = 0; i < n; ++i) h ^= t[table][i][s[i] > 0 ? 1 : 0];
+    return h;
+}
+
+int64_t energy_threshold_for_merit(int length, double f) {
+    const double l2 = static_cast<double>(length) * length;
+    return static_cast<int64_t>(std::floor(l2 / (2.0 * f)));
+}
+
+int64_t effective_iterations(int length, int64_t max_it, double mult) {
+    if (max_it > 0) return max_it;
+    return static_cast<int64_t>(mult * (length + 1) / 2);
+}
+
+int effective_prefix_len(int prefix_len, int walkers) {
+    if (prefix_len >= 0) return prefix_len;
+    int p = 1;
+    while ((1 << (p - 1)) < walkers) ++p;
+    return p;
+}
+
+void bloom_size(uint64_t capacity, double fpr, uint64_t& bits, int& k) {
+    if (capacity == 0) capacity = 1;
+    const double ln2 = std::log(2.0);
+    const double m = -static_cast<double>(capacity) * std::log(fpr) / (ln2 * ln2);
+    const auto b = static_cast<uint64_t>(std::ceil(m));
+    k = static_cast<int>(std::lround(m / static_cast<double>(capacity) * ln2));
+    if (k < 1) k = 1;
+    bits = b < 64 ? 64 : b;
+}
+
+std::vector<int8_t> rank_prefixes(int p) {
+    const uint32_t count = 1u << (p - 1);
+    std::vector<std::pair<int64_t, uint32_t>> order(count);
+    for (uint32_t code = 0; code < count; ++code) {
+        int8_t s[32];
+        s[0] = 1;
+        for (int j = 1; j < p; ++j) s[j] = ((code >> (j - 1)) & 1) ? -1 : 1;
+        int64_t pot = 0;  // prefix_potential (saw.cpp:11-20)
+        for (int lag = 1; lag < p; ++lag) {
+            int64_t c = 0;
+            for (int i = 0; i + lag < p; ++i) c += s[i] * s[i + lag];
+            pot += c * c;
+        }
+        order[code] = {pot, code};
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<int8_t> out(static_cast<size_t>(count) * p);
+    for (uint32_t r = 0; r < count; ++r) {
+        const uint32_t code = order[r].second;
+        int8_t* s = &out[static_cast<size_t>(r) * p];
+        s[0] = 1;
+        for (int j = 1; j < p; ++j) s[j] = ((code >> (j - 1)) & 1) ? -1 : 1;
+    }
+    return out;
+}
+
+void expand_skew(const int8_t* half, int kp1, int8_t* full) {
+    const int k = kp1 - 1;
+    std::copy(half, half + kp1, full);
+    for (int i = 1; i <= k; ++i) full[k + i] = (i & 1) ? static_cast<int8_t>(-full[k - i]) : full[k - i];
+}
+
+std::string hex_encode(const int8_t* s, int n) {
+    static const char* kHex = "0123456789ABCDEF";
+    const int digits = (n + 3) / 4;
+    const int pad = digits * 4 - n;
+    std::string out(static_cast<size_t>(digits), '0');
+    for (int d = 0; d < digits; ++d) {
+        int v = 0;
+        for (int b = 0; b < 4; ++b) {
+            const int pos = 4 * d + b - pad;
+            v = (v << 1) | ((pos >= 0 && s[pos] > 0) ? 1 : 0);
+        }
+        out[static_cast<size_t>(d)] = kHex[v];
+    }
+    return out;
+}
+
+std::string format_record(const int8_t* s, int n, int64_t energy) {
+    char fbuf[40];
+    std::snprintf(fbuf, sizeof fbuf, "%.4f",
+                  static_cast<double>(n) * static_cast<double>(n) / (2.0 * static_cast<double>(energy)));
+    std::string line = std::to_string(n);
+    line += '\t';
+    line += std::to_string(energy);
+    line += '\t';
+    line += fbuf;
+    line += '\t';
+    line += hex_encode(s, n);
+    line += "\tsaw";
+    return line;
+}
+
+std::string derive(const labs_saw_config& cfg, Derived& d) {
+    const int L = cfg.length;
+    if (L < 3 || L % 2 == 0) return "saw: length must be odd and >= 3";
+    if (cfg.walkers < 1) return "saw: walkers must be >= 1";
+    d.e_l = cfg.target_merit > 0.0 ? energy_threshold_for_merit(L, cfg.target_merit)
+                                   : cfg.energy_threshold;
+    if (d.e_l <= 0) return "saw: energy threshold E_l must be positive";
+    d.t_i = effective_iterations(L, cfg.max_iterations, cfg.ti_multiplier);
+    if (d.t_i < 1) return "saw: T_i must be >= 1";
+    d.L = L;
+    d.k = (L - 1) / 2;
+    d.kp1 = d.k + 1;
+    d.p = effective_prefix_len(cfg.prefix_len, cfg.walkers);
+    if (d.p > d.kp1) return "saw: prefix length exceeds half length k+1";
+    if (cfg.max_restarts == 0 && cfg.time_budget_s <= 0 && cfg.candidate_quota == 0 &&
+        cfg.stop_at_energy == 0)
+        return "saw: no stop condition configured";
+    if (cfg.bloom_fpr <= 0 || cfg.bloom_fpr >= 1) return "BloomFilter: fpr must be in (0,1)";
+    if (d.p > 30) return "rank_prefixes: p > 30 is not enumerable";
+    if (d.kp1 > kMaxHalf) return "saw: length exceeds the tabulation hash range (k+1 <= 1024)";
+    bloom_size(static_cast<uint64_t>(d.t_i) + 1, cfg.bloom_fpr, d.bloom_bits, d.bloom_k);
+    if (d.p == 0) {
+        d.nprefix = 1;
+        d.prefixes.clear();
+        d.prefix_bits.assign(1, 0u);
+    } else {
+        d.nprefix = 1 << (d.p - 1);
+        d.prefixes = rank_prefixes(d.p);
+        d.prefix_bits.assign(static_cast<size_t>(d.nprefix), 0u);
+        for (int c = 0; c < d.nprefix; ++c)
+            for (int j = 0; j < d.p; ++j)
+                if (d.prefixes[static_cast<size_t>(c) * d.p + j] > 0) d.prefix_bits[c] |= 1u << j;
+    }
+    return "";
+}
+
+static int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bloom_bits,
+                             int bloom_k, WalkParams& wp) {
+    wp = WalkParams{};
+    wp.L = L;
+    wp.k = (L - 1) / 2;
+    wp.kp1 = wp.k + 1;
+    wp.p = p;
+    const int free_bits = wp.kp1 - p;
+    wp.R = std::max(1, (free_bits + 31) / 32);
+    if (wp.R > kMaxR) return "saw: more than 512 free half bits is not supported by the GPU path";
+    wp.S = std::max(1, (wp.k + 3) / 4);
+    if (wp.S > 128) return "saw: length too large for the GPU path";
+    wp.off = 4 * wp.S + 8;
+    const int amax_h = (p + 32 * wp.R) / 2 + 1;
+    int nwp = std::max((wp.off + amax_h + 1) / 4 + wp.S + wp.R + 3, (wp.off + wp.k) / 4 + wp.k / 4 + 4);
+    nwp = round_up(nwp, 4);
+    while (nwp % 32 != 16) nwp += 4;  // parity arrays start on different bank halves
+    wp.nwp = nwp;
+    wp.hw = (wp.kp1 + 31) / 32;
+    if (bloom_bits >= (1ull << 32)) return "saw: Bloom filter exceeds 2^32 bits";
+    if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";
+    wp.bloom_bits = static_cast<uint32_t>(bloom_bits);
+    wp.bloom_k = bloom_k;
+    wp.bloom_words = round_up(static_cast<int>((bloom_bits + 31) / 32), 4);
+    wp.bloom_mu = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / bloom_bits);
+    wp.t_i = t_i;
+    wp.e_l = e_l;
+    const int s4 = round_up(wp.S, 4);
+    wp.off_c8 = 2 * nwp;
+    wp.off_c16 = wp.off_c8 + s4;
+    wp.off_half = wp.off_c16 + 2 * s4;
+    wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
+    wp.warp_words = wp.off_bloom + wp.bloom_words;
+    const int fm_words = round_up(2 * wp.kp1 * 2, 4);
+    int wpb = 4;
+    while (wpb > 1 && (fm_words + wpb * wp.warp_words) * 4 > 227 * 1024) --wpb;
+    if ((fm_words + wpb * wp.warp_words) * 4 > 227 * 1024)
+        return "saw: per-walk state (Bloom filter) exceeds shared memory; lower T_i or raise "
+               "--bloom-fpr";
+    wp.warps_per_block = wpb;
+    wp.rec_words = kRecHeader + wp.hw;
+    return "";
+}
+
+}  // namespace labs_b200

@@ -1,0 +1,86 @@
+// saw_device.h -- plain-old-data shared by the host orchestration (C++) and the
+// sm_100a kernels.  No torch or CUDA types, so it is usable from both sides.
+#pragma once
+#include <stdint.h>
+
+namespace labs_b200 {
+
+constexpr int kMaxR = 16;          // neighbours per lane: free bits <= 32*16 = 512
+constexpr int kMaxHalf = 1024;     // TabulationHash::kMaxLen (rng.hpp:77)
+constexpr int kRecHeader = 4;      // record header words: walk, iteration, energy, flags
+
+// Derived, device-ready description of one Step-1 launch (one batch of walks).
+struct WalkParams {
+    int32_t L, k, kp1, p;          // L = 2k+1, half length k+1, prefix length p
+    int32_t S;                     // 4-lag steps covering even lags t=1..k
+    int32_t R;                     // free neighbours per lane
+    int32_t nwp;                   // 32-bit words per parity byte-array
+    int32_t off;                   // byte offset of logical index 0 in a parity array
+    int32_t hw;                    // 32-bit words per packed half
+    int32_t bloom_k;               // hashes per key
+    uint32_t bloom_bits;           // m
+    int32_t bloom_words;           // ceil(m/32) rounded to 4
+    uint64_t bloom_mu;             // floor(2^64 / m) (Barrett)
+    int64_t t_i;                   // iteration cap
+    int64_t e_l;                   // sieve: emit iff E < e_l
+    int32_t warp_words;            // shared-memory words per walk (warp)
+    int32_t off_c8, off_c16, off_half, off_bloom;  // word offsets inside a warp's slice
+    int32_t warps_per_block;
+    int32_t debug_check;           // re-derive E from C every iteration, flag divergence
+    int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)
+    int32_t rec_words;             // kRecHeader + hw
+    int64_t nwalks;                // walks in this launch
+    int64_t rec_cap;               // record slots in rec
+    // inputs (device pointers)
+    const uint64_t* fm;            // [2][kp1] tabulation flip masks
+    const uint64_t* tab;           // [2][kp1][2] tabulation entries
+    uint64_t salt0, salt1;         // length salts for kp1
+    const uint32_t* halves;        // [nwalks][hw] initial half bits (bit i set <=> +1)
+    // outputs
+    uint32_t* rec;                 // [rec_cap][rec_words]
+    unsigned long long* rec_count; // emissions attempted (may exceed rec_cap => overflow)
+    int64_t* walk_stats;           // [nwalks][kWalkStatWords]
+};
+
+// per-walk stats record (int64 words)
+enum WalkStat : int {
+    kWsIterations = 0,
+    kWsEmitted = 1,
+    kWsBest = 2,
+    kWsInitial = 3,
+    kWsExhausted = 4,
+    kWsDeltaEvals = 5,    // unvisited free neighbours evaluated (count_visited=1 only)
+    kWsVisitedProbes = 6, // lazy-mode Bloom probe rounds
+    kWsWideIters = 7,     // iterations that needed the int16 correlation path
+    kWsDiverged = 8,      // debug_check failures
+    kWalkStatWords = 9
+};
+
+// One seed segment = restarts [r0, r0+restarts) of one walker, drawn in order
+// from the walker's xoshiro stream (state carried across segments).
+struct SeedParams {
+    int32_t kp1, p, hw, nseg;
+    uint64_t seed;
+    const uint32_t* walker_ids;    // [nseg] global walker index (RNG stream)
+    const uint32_t* prefix_bits;   // [nseg] pinned prefix bits (bit i set <=> +1)
+    const int64_t* seg_restarts;   // [nseg]
+    const int64_t* seg_offset;     // [nseg] first walk index of the segment in `halves`
+    const int32_t* seg_init;       // [nseg] 1 = fresh Rng(seed, walker)
+    uint64_t* rng_state;           // [nseg][4] in/out
+    uint32_t* halves;              // [nwalks][hw]
+};
+
+struct EnumParams {
+    int32_t L, k, kp1, p, m;       // Gray range over half positions [p, p+m)
+    int32_t chunk_log2;            // 2^chunk_log2 Gray steps per warp task
+    int32_t hw;
+    int64_t e_l;
+    uint64_t g_begin, g_end;       // configuration index range
+    const uint32_t* base_half;     // [hw] half bits of configuration 0
+    uint32_t* rec;                 // [rec_cap][2] (g lo, g hi) + energy -> 4 words
+    int64_t rec_cap;
+    unsigned long long* rec_count;
+    int64_t* best;                 // [nchunks][2] best energy, best g
+};
+
+}  // namespace labs_b200

@@ -1,0 +1,254 @@
+// labs -- command-line driver of the B200 Step-1 engine.
+//
+// Keeps the reference CLI's `saw` subcommand surface and output byte-for-byte
+// (tools/labs_main.cpp:53-62, 95-106, 184-199): the same flags, the stderr
+// summary "walks= iterations= emitted= bestE= wall=...s" and TSV records
+// (format_record) on stdout or into --out.  GPU controls are additive:
+// --gpus N, --device D, --count-visited, --stats-json.
+//
+// Extension subcommand `enumerate` runs the restriction-class Gray enumeration.
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "labs_b200.hpp"
+
+namespace {
+
+int default_threads() {  // labs_main.cpp:21-28
+    if (const char* env = std::getenv("LABS_THREADS")) {
+        const int n = std::atoi(env);
+        if (n >= 1) return n;
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    return hc ? static_cast<int>(hc) : 1;
+}
+
+// Minimal CLI11-compatible option parsing: --opt v, --opt=v, -L v, -Lv, flags.
+class Args {
+public:
+    Args(int argc, char** argv, int first) {
+        for (int i = first; i < argc; ++i) toks_.emplace_back(argv[i]);
+    }
+    // returns false and sets error on malformed input
+    bool parse(const std::map<std::string, std::string*>& opts,
+               const std::map<std::string, bool*>& flags, std::string& err) {
+        for (size_t i = 0; i < toks_.size(); ++i) {
+            std::string t = toks_[i], val;
+            bool has_val = false;
+            if (t.rfind("--", 0) == 0) {
+                const auto eq = t.find('=');
+                if (eq != std::string::npos) {
+                    val = t.substr(eq + 1);
+                    t = t.substr(0, eq);
+                    has_val = true;
+                }
+            } else if (t.size() > 2 && t[0] == '-' && t[1] != '-') {
+                val = t.substr(2);
+                if (!val.empty() && val[0] == '=') val = val.substr(1);
+                t = t.substr(0, 2);
+                has_val = true;
+            }
+            auto f = flags.find(t);
+            if (f != flags.end()) {
+                *f->second = true;
+                continue;
+            }
+            auto o = opts.find(t);
+            if (o == opts.end()) {
+                err = "The following argument was not expected: " + toks_[i];
+                return false;
+            }
+            if (!has_val) {
+                if (i + 1 >= toks_.size()) {
+                    err = t + " requires an argument";
+                    return false;
+                }
+                val = toks_[++i];
+            }
+            *o->second = val;
+        }
+        return true;
+    }
+
+private:
+    std::vector<std::string> toks_;
+};
+
+class FileSink final : public labs_b200::CandidateSink {  // labs_main.cpp:30-43
+public:
+    explicit FileSink(const std::string& path) : out_(path) {
+        if (!out_) throw std::runtime_error("cannot open output file: " + path);
+    }
+    void emit(const labs_b200::Candidate& c) override { out_ << labs_b200::format_record(c) << '\n'; }
+
+private:
+    std::ofstream out_;
+};
+
+long long to_ll(const std::string& s, const char* name) {
+    char* end = nullptr;
+    const long long v = std::strtoll(s.c_str(), &end, 10);
+    if (s.empty() || *end) throw std::invalid_argument(std::string(name) + ": not an integer: " + s);
+    return v;
+}
+double to_d(const std::string& s, const char* name) {
+    char* end = nullptr;
+    const double v = std::strtod(s.c_str(), &end);
+    if (s.empty() || *end) throw std::invalid_argument(std::string(name) + ": not a number: " + s);
+    return v;
+}
+
+int cmd_saw(int argc, char** argv) {
+    labs_b200::SawConfig saw;
+    saw.threads = default_threads();
+    std::map<std::string, std::string> v;
+    const char* names[] = {"--length", "--walkers", "--p", "--ti", "--ti-mult", "--el",
+                           "--target-f", "--restarts", "--bloom-fpr", "--seconds", "--quota",
+                           "--stop-at-energy", "--seed", "--threads", "--out", "--gpus",
+                           "--device", "--stats-json"};
+    std::map<std::string, std::string*> opts;
+    for (const char* n : names) opts[n] = &v[n];
+    opts["-L"] = &v["--length"];
+    bool count_visited = false, help = false;
+    std::map<std::string, bool*> flags{{"--count-visited", &count_visited}, {"--help", &help},
+                                       {"-h", &help}};
+    Args a(argc, argv, 2);
+    std::string err;
+    if (!a.parse(opts, flags, err)) {
+        std::cerr << err << "\nRun with --help for more information.\n";
+        return 109;
+    }
+    if (help) {
+        std::cout << "labs saw -L <odd L> [--walkers N] [--p P] [--ti T] [--ti-mult M] [--el E] "
+                     "[--target-f F] [--restarts R] [--bloom-fpr X] [--seconds S] [--quota Q] "
+                     "[--stop-at-energy E] [--seed S] [--threads N] [--out FILE] [--gpus N] "
+                     "[--device D] [--count-visited] [--stats-json FILE]\n";
+        return 0;
+    }
+    if (v["--length"].empty()) {
+        std::cerr << "--length is required\nRun with --help for more information.\n";
+        return 106;
+    }
+    saw.length = static_cast<int>(to_ll(v["--length"], "--length"));
+    if (!v["--walkers"].empty()) saw.walkers = static_cast<int>(to_ll(v["--walkers"], "--walkers"));
+    if (!v["--p"].empty()) saw.prefix_len = static_cast<int>(to_ll(v["--p"], "--p"));
+    if (!v["--ti"].empty()) saw.max_iterations = to_ll(v["--ti"], "--ti");
+    if (!v["--ti-mult"].empty()) saw.ti_multiplier = to_d(v["--ti-mult"], "--ti-mult");
+    if (!v["--el"].empty()) saw.energy_threshold = to_ll(v["--el"], "--el");
+    if (!v["--target-f"].empty()) saw.target_merit = to_d(v["--target-f"], "--target-f");
+    if (!v["--restarts"].empty()) saw.max_restarts = to_ll(v["--restarts"], "--restarts");
+    if (!v["--bloom-fpr"].empty()) saw.bloom_fpr = to_d(v["--bloom-fpr"], "--bloom-fpr");
+    if (!v["--seconds"].empty()) saw.time_budget_s = to_d(v["--seconds"], "--seconds");
+    if (!v["--quota"].empty()) saw.candidate_quota = to_ll(v["--quota"], "--quota");
+    if (!v["--stop-at-energy"].empty())
+        saw.stop_at_energy = to_ll(v["--stop-at-energy"], "--stop-at-energy");
+    if (!v["--seed"].empty()) saw.seed = static_cast<std::uint64_t>(to_ll(v["--seed"], "--seed"));
+    if (!v["--threads"].empty()) saw.threads = static_cast<int>(to_ll(v["--threads"], "--threads"));
+    if (!v["--gpus"].empty()) saw.gpus = static_cast<int>(to_ll(v["--gpus"], "--gpus"));
+    if (!v["--device"].empty()) saw.device = static_cast<int>(to_ll(v["--device"], "--device"));
+    saw.count_visited = count_visited;
+
+    labs_b200::CollectingSink collect;  // labs_main.cpp:184-199
+    std::unique_ptr<FileSink> file;
+    labs_b200::CandidateSink* sink = &collect;
+    if (!v["--out"].empty()) {
+        file = std::make_unique<FileSink>(v["--out"]);
+        sink = file.get();
+    }
+    const auto stats = labs_b200::run_saw_pool(saw, *sink);
+    std::cerr << "walks=" << stats.walks << " iterations=" << stats.iterations
+              << " emitted=" << stats.emitted << " bestE=" << stats.best_energy
+              << " wall=" << stats.wall_seconds << "s\n";
+    if (v["--out"].empty())
+        for (const auto& c : collect.take()) std::cout << labs_b200::format_record(c) << '\n';
+    if (!v["--stats-json"].empty()) {
+        std::ofstream js(v["--stats-json"]);
+        const auto& g = stats.gpu;
+        js << "{\"walks\": " << g.walks << ", \"iterations\": " << g.iterations
+           << ", \"emitted\": " << g.emitted << ", \"emitted_raw\": " << g.emitted_raw
+           << ", \"best_energy\": " << g.best_energy << ", \"delta_evals\": " << g.delta_evals
+           << ", \"delta_evals_computed\": " << g.delta_evals_computed
+           << ", \"kernel_ms\": " << g.kernel_ms << ", \"seed_ms\": " << g.seed_ms
+           << ", \"wall_seconds\": " << g.wall_seconds << ", \"n_gpus\": " << g.n_gpus << "}\n";
+    }
+    return 0;
+}
+
+int cmd_enumerate(int argc, char** argv) {
+    std::map<std::string, std::string> v;
+    std::map<std::string, std::string*> opts;
+    for (const char* n : {"--length", "--p", "--class", "--free", "--el", "--target-f", "--out"})
+        opts[n] = &v[n];
+    opts["-L"] = &v["--length"];
+    std::map<std::string, bool*> flags;
+    Args a(argc, argv, 2);
+    std::string err;
+    if (!a.parse(opts, flags, err)) {
+        std::cerr << err << '\n';
+        return 109;
+    }
+    const int L = static_cast<int>(to_ll(v["--length"], "--length"));
+    const int p = static_cast<int>(to_ll(v["--p"].empty() ? "12" : v["--p"], "--p"));
+    const int cls = static_cast<int>(to_ll(v["--class"].empty() ? "0" : v["--class"], "--class"));
+    const int m = static_cast<int>(to_ll(v["--free"], "--free"));
+    long long el = v["--el"].empty() ? 0 : to_ll(v["--el"], "--el");
+    if (!v["--target-f"].empty()) {
+        const double f = to_d(v["--target-f"], "--target-f");
+        el = static_cast<long long>(static_cast<double>(L) * L / (2.0 * f));
+    }
+    struct Ctx {
+        std::ostream* out;
+        int L;
+    };
+    std::ofstream fo;
+    std::ostream* out = &std::cout;
+    if (!v["--out"].empty()) {
+        fo.open(v["--out"]);
+        out = &fo;
+    }
+    Ctx ctx{out, L};
+    labs_enum_stats st{};
+    const int rc = labs_enumerate_class(
+        L, p, cls, m, el, 0, 1ull << m,
+        [](void* u, uint64_t g, int64_t e) -> int {
+            auto* c = static_cast<Ctx*>(u);
+            *c->out << g << '\t' << e << '\n';
+            return 0;
+        },
+        &ctx, &st);
+    if (rc != LABS_OK) labs_b200::throw_status(rc);
+    std::cerr << "configurations=" << st.configurations << " emitted=" << st.emitted
+              << " bestE=" << st.best_energy << " best_g=" << st.best_g
+              << " kernel_ms=" << st.kernel_ms << '\n';
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::cerr << "A subcommand is required\nRun with --help for more information.\n";
+        return 106;
+    }
+    const std::string sub = argv[1];
+    try {
+        if (sub == "saw") return cmd_saw(argc, argv);
+        if (sub == "enumerate") return cmd_enumerate(argc, argv);
+        if (sub == "--help" || sub == "-h") {
+            std::cout << "labs {saw, enumerate} ... (B200 Step-1 engine)\n";
+            return 0;
+        }
+        std::cerr << "The following argument was not expected: " << sub << '\n';
+        return 109;
+    } catch (const std::exception& ex) {  // labs_main.cpp:304-307
+        std::cerr << "error: " << ex.what() << '\n';
+        return 1;
+    }
+}
