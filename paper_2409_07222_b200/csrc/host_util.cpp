@@ -176,12 +176,18 @@ std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bl
     if (wp.R > kMaxR) return "saw: more than 512 free half bits is not supported by the GPU path";
     wp.S = std::max(1, (wp.k + 3) / 4);
     if (wp.S > 128) return "saw: length too large for the GPU path";
-    wp.off = 4 * wp.S + 8;
+    wp.nwx = (wp.kp1 + 3) / 4;
+    // X arrays: backward reads down to index -(4S+4) (C update), forward reads up to
+    // k/2 + 4S + 8 (C update), 4*nwx (main loop) and 4*(nwx+S+2) (correlation init).
+    wp.xoff = 4 * wp.S + 8;
+    const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3)});
+    wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
+    // kernel: main loop reads d in [-(p+32R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4S+4
     const int amax_h = (p + 32 * wp.R) / 2 + 1;
-    int nwp = std::max((wp.off + amax_h + 1) / 4 + wp.S + wp.R + 3, (wp.off + wp.k) / 4 + wp.k / 4 + 4);
-    nwp = round_up(nwp, 4);
-    while (nwp % 32 != 16) nwp += 4;  // parity arrays start on different bank halves
-    wp.nwp = nwp;
+    int koff = std::max(amax_h + 4 * wp.R + 12, 4 * wp.S + 12);
+    while (koff % 4 != 3) ++koff;
+    wp.koff = koff;
+    wp.kwords = round_up((koff + std::max(4 * wp.nwx, 4 * wp.S) + 16) / 4, 4);
     wp.hw = (wp.kp1 + 31) / 32;
     if (bloom_bits >= (1ull << 32)) return "saw: Bloom filter exceeds 2^32 bits";
     if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";
@@ -191,10 +197,15 @@ std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bl
     wp.bloom_mu = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / bloom_bits);
     wp.t_i = t_i;
     wp.e_l = e_l;
-    const int s4 = round_up(wp.S, 4);
-    wp.off_c8 = 2 * nwp;
-    wp.off_c16 = wp.off_c8 + s4;
-    wp.off_half = wp.off_c16 + 2 * s4;
+    // X0 and X1 start on different bank halves (lanes of both parities read each step)
+    int x1 = wp.xwords;
+    while (x1 % 32 != 16) x1 += 4;
+    wp.off_x1 = x1;
+    wp.off_kl = wp.off_x1 + wp.xwords;
+    wp.off_kh = wp.off_kl + wp.kwords;
+    wp.off_c16 = wp.off_kh + wp.kwords;
+    wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
+    wp.off_half = wp.off_kq + round_up(wp.kp1, 4);
     wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
     wp.warp_words = wp.off_bloom + wp.bloom_words;
     const int fm_words = round_up(2 * wp.kp1 * 2, 4);

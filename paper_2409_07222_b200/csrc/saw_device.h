@@ -10,12 +10,20 @@ constexpr int kMaxHalf = 1024;     // TabulationHash::kMaxLen (rng.hpp:77)
 constexpr int kRecHeader = 4;      // record header words: walk, iteration, energy, flags
 
 // Derived, device-ready description of one Step-1 launch (one batch of walks).
+// Per-walk shared-memory layout (32-bit word offsets inside a warp's slice):
+//   X0, X1 : parity arrays, byte xoff+i = x_{2i+parity} in {-1,+1}, 0 = padding
+//   KL, KH : symmetric correlation kernel, byte koff+d = low / high byte of C_{2|d|}
+//            (KH only maintained while some |C| > 127)
+//   C16    : int16 C_{2t}, t = 1..4S (pairs per word)
+//   KQ     : int32 per half index a: 16 N(a) + 32 Q(a)  (a < k),  4 N + 8 Q (a = k)
+//   HALF   : packed current half,  BLOOM : visited filter bits
 struct WalkParams {
     int32_t L, k, kp1, p;          // L = 2k+1, half length k+1, prefix length p
-    int32_t S;                     // 4-lag steps covering even lags t=1..k
+    int32_t S;                     // 4-lag words covering even lags t=1..k (C update)
     int32_t R;                     // free neighbours per lane
-    int32_t nwp;                   // 32-bit words per parity byte-array
-    int32_t off;                   // byte offset of logical index 0 in a parity array
+    int32_t nwx;                   // 4-position words per parity array (main loop trip count)
+    int32_t xoff, xwords;          // X array byte offset of index 0, words per array
+    int32_t koff, kwords;          // kernel byte offset of d = 0 (== 3 mod 4), words per array
     int32_t hw;                    // 32-bit words per packed half
     int32_t bloom_k;               // hashes per key
     uint32_t bloom_bits;           // m
@@ -24,7 +32,7 @@ struct WalkParams {
     int64_t t_i;                   // iteration cap
     int64_t e_l;                   // sieve: emit iff E < e_l
     int32_t warp_words;            // shared-memory words per walk (warp)
-    int32_t off_c8, off_c16, off_half, off_bloom;  // word offsets inside a warp's slice
+    int32_t off_x1, off_kl, off_kh, off_c16, off_kq, off_half, off_bloom;  // X0 at 0
     int32_t warps_per_block;
     int32_t debug_check;           // re-derive E from C every iteration, flag divergence
     int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)

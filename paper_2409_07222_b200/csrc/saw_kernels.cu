@@ -12,14 +12,17 @@
 //
 // Arithmetic.  For a skew-symmetric pivot the four sign products of
 // the reference's fused delta pair up (x_b x_{b+-kk} = x_a x_{a-+kk}), so for half
-// index a < k:
-//     dE(a) = 16 N(a) + 32 Q(a) - 8 x_a (DP(a) - 2 Csum) + 8 (-1)^(k-a) C_{k-a}
-// and for the centre a = k:  dE = 4 N + 8 Q - 4 x_k (DP - 2 Csum), with
-//     DP(a) = sum_t C_{2t} (y_{a-2t} + y_{a+2t}),  y = x + 1 in {0,1,2}, 1 = padding,
-//     Csum = sum_t C_{2t},  N(a) = #valid single terms,  Q(a) = sum_t x_{a-2t} x_{a+2t}.
-// DP is the only O(L) part: 4 lags per IDP4A on byte-packed y words (int8 C), or per
-// two IDP2A (int16 C) while some |C| > 127.  Q is maintained incrementally (O(1) per
-// neighbour per flip).  Everything is exact integer arithmetic.
+// index a < k (b = L-1-a):
+//     dE(a) = 16 N(a) + 32 Q(a) - 8 x_a G(a) + 8 (-1)^(k-a) C_{2(k-a)}
+// and for the centre a = k:  dE = 4 N + 8 Q - 4 x_k G, where
+//     G(a) = sum_{j = a mod 2, j != a} C_{|a-j|} x_j      (x = 0 outside [0, L))
+//     N(a) = #valid single terms,  Q(a) = sum_t x_{a-2t} x_{a+2t} (b excluded).
+// G is the only O(L) part.  On the parity array X_par it is a sliding dot product with
+// the symmetric kernel K[d] = C_{2|d|}: G(a) = sum_i X_par[i] K[i - a/2].  A lane owns
+// neighbours a0, a0+8, ..., so one X word is shared by its R neighbours and the kernel
+// window slides by one word per neighbour: 4 positions per IDP4A (int8 C), plus a
+// second IDP4A on the high bytes while some |C| > 127.  16N+32Q is kept per neighbour
+// in shared memory and updated in O(1) per flip.  Everything is exact integer math.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,6 +31,7 @@
 namespace labs_b200 {
 
 #define FULLMASK 0xffffffffu
+#define INT_BIG 0x7fffffff
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return __byte_perm(a, b, sel);
@@ -60,88 +64,89 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
     return v;
 }
 
-// y = x+1 byte -> x in {-1,0,1} per byte (no inter-byte carries: y+0x7F <= 0x81)
-__device__ __forceinline__ uint32_t y_to_x(uint32_t y) { return (y + 0x7F7F7F7Fu) ^ 0x80808080u; }
+__device__ __forceinline__ uint32_t sel4(int o) {  // bytes o..o+3 of a word pair
+    return (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+}
+__device__ __forceinline__ uint32_t sel4r(int o) {  // bytes o+3..o (reversed)
+    return (uint32_t)((o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
+}
+// sign-extended byte b of w
+__device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
 
 // ---------------------------------------------------------------------------
-// Main O(L) loop: DP(a) for this lane's R neighbours a = a0 + 8m.
-// Fw: this lane's parity array (32-bit words).  Forward bytes for neighbour m at
-// step s live in words wF+s+m (+1), backward bytes in words wB+m-s (+1); the
-// PRMT'd forward/backward words slide by one word per step, so each new step
-// loads one forward and one backward word and reuses the rest from registers.
+// Main O(L) loop: G(a) for this lane's R neighbours a = a0 + 8m (a' = a0' + 4m).
+// Step w: X word w (positions 4w..4w+3 of the lane's parity) is shared by all R
+// neighbours; neighbour m needs kernel bytes koff + 4(w-m) - a0' .. +3, i.e. the
+// PRMT-aligned word KW_{w-m}; KW slides one slot per step (one new raw word).
 template <int R, bool WIDE>
-__device__ __forceinline__ void dp_step(const uint32_t* __restrict__ Fw,
-                                        const uint32_t* __restrict__ Cw, int s, int j, int wF,
-                                        int wB, uint32_t selF, uint32_t selB, uint32_t (&PF)[R],
-                                        uint32_t (&PB)[R], uint32_t& rfl, uint32_t& rbf,
-                                        int (&acc)[R]) {
-    uint32_t c0, c1;
-    if (WIDE) {
-        const uint2 cc = *reinterpret_cast<const uint2*>(Cw + 2 * s);
-        c0 = cc.x;
-        c1 = cc.y;
-    } else {
-        c0 = Cw[s];
-        c1 = 0;
-    }
-    const uint32_t nf = Fw[wF + s + R + 1];
-    const uint32_t nb = Fw[wB - s - 1];
+__device__ __forceinline__ void g_step(const uint32_t* __restrict__ Xw,
+                                       const uint32_t* __restrict__ Kl,
+                                       const uint32_t* __restrict__ Kh, int w, int j, int kb,
+                                       uint32_t sel, uint32_t (&KL)[R], uint32_t (&KH)[R],
+                                       uint32_t& rl, uint32_t& rh, int (&acc)[R],
+                                       int (&acch)[R]) {
+    const uint32_t x = Xw[w];
+    const uint32_t nl = Kl[kb + w + 2];
+    uint32_t nh = 0;
+    if (WIDE) nh = Kh[kb + w + 2];
 #pragma unroll
     for (int m = 0; m < R; ++m) {
-        const uint32_t y = PF[(j + m) % R] + PB[(m - j + R) % R];
-        if (WIDE) {
-            acc[m] = __dp2a_lo((int)c0, (int)y, acc[m]);
-            acc[m] = __dp2a_hi((int)c1, (int)y, acc[m]);
-        } else {
-            acc[m] = __dp4a((int)y, (int)c0, acc[m]);
-        }
+        acc[m] = __dp4a((int)x, (int)KL[(j - m + R) % R], acc[m]);
+        if (WIDE) acch[m] = __dp4a((int)x, (int)KH[(j - m + R) % R], acch[m]);
     }
-    PF[j] = prmt(rfl, nf, selF);
-    rfl = nf;
-    PB[(R - 1 - j) % R] = prmt(nb, rbf, selB);
-    rbf = nb;
+    KL[(j + 1) % R] = prmt(rl, nl, sel);
+    rl = nl;
+    if (WIDE) {
+        KH[(j + 1) % R] = prmt(rh, nh, sel);
+        rh = nh;
+    }
 }
 
 template <int R, bool WIDE>
-__device__ __forceinline__ void dp_neighbours(const uint32_t* __restrict__ Fw,
-                                              const uint32_t* __restrict__ Cw, int S, int wF,
-                                              int wB, uint32_t selF, uint32_t selB,
-                                              int (&acc)[R]) {
-    uint32_t PF[R], PB[R];
+__device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
+                                             const uint32_t* __restrict__ Kl,
+                                             const uint32_t* __restrict__ Kh, int nwx, int kb,
+                                             uint32_t sel, int (&acc)[R], int (&acch)[R]) {
+    uint32_t KL[R], KH[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-        PF[q] = prmt(Fw[wF + q], Fw[wF + q + 1], selF);
-        PB[q] = prmt(Fw[wB + q], Fw[wB + q + 1], selB);
-        acc[q] = 0;
+    for (int m = 0; m < R; ++m) {
+        KL[(R - m) % R] = prmt(Kl[kb - m], Kl[kb - m + 1], sel);
+        if (WIDE) KH[(R - m) % R] = prmt(Kh[kb - m], Kh[kb - m + 1], sel);
+        acc[m] = 0;
+        acch[m] = 0;
     }
-    uint32_t rfl = Fw[wF + R];
-    uint32_t rbf = Fw[wB];
-    const int nfull = (S / R) * R;
-    for (int s0 = 0; s0 < nfull; s0 += R) {
+    uint32_t rl = Kl[kb + 1], rh = 0;
+    if (WIDE) rh = Kh[kb + 1];
+    const int nfull = (nwx / R) * R;
+    for (int w0 = 0; w0 < nfull; w0 += R) {
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            dp_step<R, WIDE>(Fw, Cw, s0 + j, j, wF, wB, selF, selB, PF, PB, rfl, rbf, acc);
+            g_step<R, WIDE>(Xw, Kl, Kh, w0 + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
     }
-    if (nfull < S) {
+    if (nfull < nwx) {
 #pragma unroll
         for (int j = 0; j < R; ++j)
-            if (nfull + j < S)
-                dp_step<R, WIDE>(Fw, Cw, nfull + j, j, wF, wB, selF, selB, PF, PB, rfl, rbf, acc);
+            if (nfull + j < nwx)
+                g_step<R, WIDE>(Xw, Kl, Kh, nfull + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
     }
 }
 
 // ---------------------------------------------------------------------------
 struct WarpSmem {
-    uint32_t* F;      // [2][nwp] parity byte arrays (y = x+1, pad 1)
-    uint8_t* Fb;
-    uint32_t* C8;     // [S] int8 x4 packed C_{2t}, t = 4s+1..4s+4
-    uint32_t* C16;    // [2S] int16 x2 packed
-    uint32_t* half;   // [hw] half bits
-    uint32_t* bloom;  // [bloom_words]
+    int8_t* X0;       // parity arrays (byte views, index xoff + i)
+    int8_t* X1;
+    uint32_t* X0w;
+    uint32_t* X1w;
+    uint32_t* KL;     // kernel low bytes (word view)
+    uint32_t* KH;     // kernel high bytes
+    uint32_t* C16;    // int16 C_{2t}, t = 4s+1..4s+4 in words 2s, 2s+1
+    int* KQ;          // 16N+32Q per half index
+    uint32_t* half;   // half bits
+    uint32_t* bloom;  // visited filter
 };
 
-__device__ __forceinline__ int ybyte(const WarpSmem& w, const WalkParams& P, int j) {
-    return w.Fb[(j & 1) * P.nwp * 4 + P.off + (j >> 1)];
+__device__ __forceinline__ int xval(const WarpSmem& w, const WalkParams& P, int j) {
+    return (j & 1) ? w.X1[P.xoff + (j >> 1)] : w.X0[P.xoff + (j >> 1)];
 }
 
 // Sign of full-sequence position j of the skew expansion of `half` (skew.cpp:14-26).
@@ -157,23 +162,42 @@ __device__ __forceinline__ int x_of_half(const uint32_t* half, int k, int j) {
 }
 
 // C_{2t} by direct summation over the parity arrays (sequence.cpp:8-19 restricted to
-// even lags; odd lags of a skew sequence vanish).
+// even lags; odd lags of a skew sequence vanish): sum_par sum_i X[i] X[i+t].
 __device__ __forceinline__ int corr_even_lag(const WarpSmem& w, const WalkParams& P, int t) {
     int acc = 0;
-    const int o = t & 3, dw = t >> 2;
-    const uint32_t sel = (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+    const int dw = t >> 2;
+    const uint32_t sel = sel4(t & 3);
+    const int n0 = P.xoff >> 2;
 #pragma unroll
     for (int par = 0; par < 2; ++par) {
-        const uint32_t* Fw = w.F + par * P.nwp;
-        const int imax = (P.L - 1 - par) >> 1;  // last logical index holding a real position
-        const int n0 = P.off >> 2, n1 = (P.off + imax) >> 2;
-        for (int n = n0; n <= n1; ++n) {
-            const uint32_t xa = y_to_x(Fw[n]);
-            const uint32_t xb = y_to_x(prmt(Fw[n + dw], Fw[n + dw + 1], sel));
-            acc = __dp4a((int)xa, (int)xb, acc);
-        }
+        const uint32_t* Xw = par ? w.X1w : w.X0w;
+        for (int n = n0; n < n0 + P.nwx; ++n)
+            acc = __dp4a((int)Xw[n], (int)prmt(Xw[n + dw], Xw[n + dw + 1], sel), acc);
     }
     return acc;
+}
+
+__device__ __forceinline__ uint32_t pack4(int b0, int b1, int b2, int b3) {  // low bytes
+    return prmt(prmt((uint32_t)b0, (uint32_t)b1, 0x0040), prmt((uint32_t)b2, (uint32_t)b3, 0x0040),
+                0x5410);
+}
+__device__ __forceinline__ int hi_byte(int c) { return (c - (int)(int8_t)c) >> 8; }
+
+// Store the 4 correlations c[0..3] of lag word s (t = 4s+1..4s+4) into C16 and the
+// kernel arrays: forward word (d = 4s+1..4s+4) = (c0,c1,c2,c3); mirrored word
+// (d = -4s-3..-4s) = (c2,c1,c0,cprev) with cprev = C_{2*4s} (0 for s = 0: K[0] = 0).
+__device__ __forceinline__ void store_c_word(const WarpSmem& w, const WalkParams& P, int s,
+                                             const int (&c)[4], int cprev, bool wide) {
+    w.C16[2 * s] = prmt((uint32_t)c[0], (uint32_t)c[1], 0x5410);
+    w.C16[2 * s + 1] = prmt((uint32_t)c[2], (uint32_t)c[3], 0x5410);
+    const int fw = (P.koff + 1) / 4 + s;
+    const int bw = (P.koff - 3) / 4 - s;
+    w.KL[fw] = pack4(c[0], c[1], c[2], c[3]);
+    w.KL[bw] = pack4(c[2], c[1], c[0], cprev);
+    if (wide) {
+        w.KH[fw] = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[bw] = pack4(hi_byte(c[2]), hi_byte(c[1]), hi_byte(c[0]), hi_byte(cprev));
+    }
 }
 
 template <int R, bool COUNT>
@@ -181,34 +205,35 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                               const uint64_t* fm1, int64_t walk, int lane, int* score_out,
                               int* corr_out) {
     const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
-    const int nj = (S + 31) >> 5;  // steps owned per lane (<= 4)
+    const int nj = (S + 31) >> 5;  // lag words owned per lane (<= 4)
 
-    // ---- load the initial half, build parity arrays, clear Bloom ----
+    // ---- load the initial half, build parity arrays, clear kernel + Bloom ----
     const uint32_t* src = P.halves + walk * P.hw;
     for (int i = lane; i < P.hw; i += 32) w.half[i] = src[i];
     __syncwarp();
-    for (int wi = lane; wi < 2 * P.nwp; wi += 32) {
-        const int par = wi >= P.nwp;
-        const int word = wi - par * P.nwp;
+    for (int wi = lane; wi < 2 * P.xwords; wi += 32) {
+        const int par = wi >= P.xwords;
+        const int word = wi - par * P.xwords;
         uint32_t v = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int li = word * 4 + b - P.off;
+            const int li = word * 4 + b - P.xoff;
             const int j = 2 * li + par;
-            const int y = (li >= 0 && j < L) ? x_of_half(w.half, k, j) + 1 : 1;
-            v |= (uint32_t)y << (8 * b);
+            const int x = (li >= 0 && j < L) ? x_of_half(w.half, k, j) : 0;
+            v |= ((uint32_t)x & 0xffu) << (8 * b);
         }
-        w.F[wi] = v;
+        (par ? w.X1w : w.X0w)[word] = v;
     }
+    for (int i = lane; i < 2 * P.kwords; i += 32) w.KL[i] = 0;  // KL and KH are adjacent
     {
         uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
         for (int i = lane; i < (P.bloom_words >> 2); i += 32) b4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
 
-    // ---- C_{2t} for owned steps (lanes over lags), E, Csum, max|C| ----
-    int c[4][4];
-    int e_part = 0, csum_part = 0, cmax = 0;
+    // ---- C_{2t} for owned lag words (lanes over lags), E, max|C| ----
+    int e_part = 0, cmax = 0;
+    int cw[4][4];
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
         const int s = lane + 32 * jj;
@@ -217,58 +242,45 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
             const int t = 4 * s + 1 + b;
             int v = 0;
             if (jj < nj && s < S && t <= k) v = corr_even_lag(w, P, t);
-            c[jj][b] = v;
+            cw[jj][b] = v;
             e_part += v * v;
-            csum_part += v;
             cmax = max(cmax, abs(v));
         }
     }
     int energy = warp_sum(e_part);
-    int csum = warp_sum(csum_part);
     bool wide = __reduce_max_sync(FULLMASK, (unsigned)cmax) > 127u;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
+        const int up = __shfl_up_sync(FULLMASK, cw[jj][3], 1);
+        const int wrap = __shfl_sync(FULLMASK, jj > 0 ? cw[jj > 0 ? jj - 1 : 0][3] : 0, 31);
         const int s = lane + 32 * jj;
+        const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
         if (jj < nj && s < S) {
-            const uint32_t p01 = prmt((uint32_t)c[jj][0], (uint32_t)c[jj][1], 0x0040);
-            const uint32_t p23 = prmt((uint32_t)c[jj][2], (uint32_t)c[jj][3], 0x0040);
-            w.C8[s] = prmt(p01, p23, 0x5410);
-            w.C16[2 * s] = prmt((uint32_t)c[jj][0], (uint32_t)c[jj][1], 0x5410);
-            w.C16[2 * s + 1] = prmt((uint32_t)c[jj][2], (uint32_t)c[jj][3], 0x5410);
+            store_c_word(w, P, s, cw[jj], cprev, wide);
             if (corr_out)
                 for (int b = 0; b < 4; ++b)
-                    if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = c[jj][b];
+                    if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = cw[jj][b];
         }
     }
 
-    // ---- lane geometry: neighbours a = a0 + 8m ----
+    // ---- 16N + 32Q per half index (lanes over a) ----
+    for (int a = P.p + lane; a <= k; a += 32) {
+        const int8_t* Xb = ((a & 1) ? w.X1 : w.X0) + P.xoff + (a >> 1);
+        const int tstar = (a < k) ? (k - a) : -1;
+        int q = 0;
+        for (int t = 1; 2 * t <= a; ++t)
+            if (t != tstar) q += (int)Xb[-t] * (int)Xb[t];
+        const int n = (a >> 1) + ((L - 1 - a) >> 1) - (a < k ? 1 : 0);
+        w.KQ[a] = (a < k) ? 16 * n + 32 * q : 4 * n + 8 * q;
+    }
+
+    // ---- lane geometry for the main loop ----
     const int cgrp = lane & 7, g = lane >> 3;
     const int a0 = P.p + cgrp + 8 * R * g;
     const int par = a0 & 1, a0h = a0 >> 1;
-    const uint32_t* Fw = w.F + par * P.nwp;
-    const int wF = (P.off + a0h + 1) >> 2;
-    const int oF = (P.off + a0h + 1) & 3;
-    const uint32_t selF = (uint32_t)(oF | ((oF + 1) << 4) | ((oF + 2) << 8) | ((oF + 3) << 12));
-    const int wB = (P.off + a0h - 4) >> 2;
-    const int oB = (P.off + a0h) & 3;
-    const uint32_t selB = (uint32_t)((oB + 3) | ((oB + 2) << 4) | ((oB + 1) << 8) | (oB << 12));
-
-    // ---- Q(a) for owned neighbours ----
-    int q[R];
-#pragma unroll
-    for (int m = 0; m < R; ++m) {
-        const int a = a0 + 8 * m;
-        int acc = 0;
-        if (a <= k) {
-            const uint8_t* Fb = w.Fb + par * P.nwp * 4 + P.off + (a >> 1);
-            const int tstar = (a < k) ? (k - a) : -1;
-            for (int t = 1; 2 * t <= a; ++t) {
-                if (t == tstar) continue;
-                acc += ((int)Fb[-t] - 1) * ((int)Fb[t] - 1);
-            }
-        }
-        q[m] = acc;
-    }
+    const uint32_t* Xw = (par ? w.X1w : w.X0w) + (P.xoff >> 2);
+    const int kb = (P.koff - a0h) >> 2;
+    const uint32_t ksel = sel4((P.koff - a0h) & 3);
 
     // ---- half hashes h1, h2 (saw.cpp:77-89) and the initial Bloom insert ----
     uint64_t h1 = 0, h2 = 0;
@@ -299,50 +311,47 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     const int64_t t_i = score_out ? 1 : P.t_i;
 
     for (long long it = 0; it < t_i; ++it) {
-        // ---- DP for all owned neighbours ----
-        int acc[R];
+        // ---- G for all owned neighbours ----
+        int acc[R], acch[R];
         if (wide) {
-            dp_neighbours<R, true>(Fw, w.C16, S, wF, wB, selF, selB, acc);
+            g_neighbours<R, true>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
             ++wide_iters;
         } else {
-            dp_neighbours<R, false>(Fw, w.C8, S, wF, wB, selF, selB, acc);
+            g_neighbours<R, false>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
         }
-        // ---- epilogue: exact deltas ----
+        // ---- epilogue: exact deltas (INT_BIG = not a free neighbour) ----
         int delta[R];
-        uint32_t valid = 0;
+        const int16_t* C16h = reinterpret_cast<const int16_t*>(w.C16);
+        const int8_t* Xb = (par ? w.X1 : w.X0) + P.xoff;
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int a = a0 + 8 * m;
-            delta[m] = 0;
+            int d = INT_BIG;
             if (a <= k) {
-                valid |= 1u << m;
-                const int xa = ybyte(w, P, a) - 1;
-                const int n = (a >> 1) + ((L - 1 - a) >> 1) - (a < k ? 1 : 0);
-                const int g2 = acc[m] - 2 * csum;
-                int d;
+                const int gg = wide ? acc[m] + 256 * acch[m] : acc[m];
+                const int xa = Xb[a0h + 4 * m];
+                const int kq = w.KQ[a];
                 if (a < k) {
-                    const int t = k - a;
-                    const int ct = (int)reinterpret_cast<const int16_t*>(w.C16)[t - 1];
-                    d = 16 * n + 32 * q[m] - 8 * xa * g2 + (((k - a) & 1) ? -8 : 8) * ct;
+                    const int ct = C16h[k - a - 1];
+                    d = kq - 8 * xa * gg + (((k - a) & 1) ? -8 * ct : 8 * ct);
                 } else {
-                    d = 4 * n + 8 * q[m] - 4 * xa * g2;
+                    d = kq - 4 * xa * gg;
                 }
-                delta[m] = d;
             }
+            delta[m] = d;
         }
         if (score_out) {
 #pragma unroll
             for (int m = 0; m < R; ++m)
-                if (valid >> m & 1) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
+                if (a0 + 8 * m <= k) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
             break;
         }
 
         // ---- choose: lowest (delta, hp) among unvisited (best_neighbour) ----
-        uint32_t excl = 0;
         if (COUNT) {
 #pragma unroll
             for (int m = 0; m < R; ++m) {
-                if (!(valid >> m & 1)) continue;
+                if (delta[m] == INT_BIG) continue;
                 const int a = a0 + 8 * m;
                 const uint64_t n1 = h1 ^ fm0[a], n2 = h2 ^ fm1[a];
                 bool hit = true;
@@ -353,27 +362,31 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                         break;
                     }
                 }
-                if (hit) excl |= 1u << m;
+                if (hit) delta[m] = INT_BIG;
                 else ++evals_part;
             }
         } else if (prev_hp >= 0) {
             // the undo move leads back to the previous pivot, which is in the filter
             const int r = prev_hp - P.p;
-            if ((r & 7) == cgrp && ((r >> 3) / R) == g) excl |= 1u << ((r >> 3) % R);
+            if ((r & 7) == cgrp && ((r >> 3) / R) == g) {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    if (m == ((r >> 3) % R)) delta[m] = INT_BIG;
+            }
         }
         int dstar = 0, astar = -1;
         while (true) {
-            int bd = 0x7fffffff, ba = 0x7fffffff;
+            int bd = INT_BIG, bm = 0;
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
-                if ((valid >> m & 1) && !(excl >> m & 1) && delta[m] < bd) {
+            for (int m = 0; m < R; ++m)
+                if (delta[m] < bd) {
                     bd = delta[m];
-                    ba = a0 + 8 * m;
+                    bm = m;
                 }
-            }
             const int md = __reduce_min_sync(FULLMASK, bd);
-            if (md == 0x7fffffff) break;  // every free neighbour visited
-            const int ma = __reduce_min_sync(FULLMASK, bd == md ? ba : 0x7fffffff);
+            if (md == INT_BIG) break;  // every free neighbour visited
+            const int mine = (bd == md) ? a0 + 8 * bm : INT_BIG;
+            const int ma = __reduce_min_sync(FULLMASK, mine);
             if (COUNT) {
                 dstar = md;
                 astar = ma;
@@ -387,9 +400,10 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                 bit = (w.bloom[idx >> 5] >> (idx & 31)) & 1;
             }
             if (__all_sync(FULLMASK, bit)) {
-                if (ba == ma && bd == md) {
-                    const int r = ma - P.p;
-                    excl |= 1u << ((r >> 3) % R);
+                if (mine == ma) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        if (m == bm) delta[m] = INT_BIG;
                 }
                 continue;
             }
@@ -406,84 +420,79 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
         ++iterations;
         const bool cen = astar == k;
         const int bstar = L - 1 - astar;
-        const int xa = ybyte(w, P, astar) - 1;
+        const int xa = xval(w, P, astar);
         const int xb = ((k - astar) & 1) ? -xa : xa;
+        int cn[4][4];
+        int cmx = 0, esp = 0;
         {
-            // even-lag correlation update: C_t += dc_t(astar), lanes over lags
+            // even-lag correlation update C_t += dc_t(astar), lanes over lag words
             const int ah = astar >> 1, apar = astar & 1;
-            const uint32_t* Fa = w.F + apar * P.nwp;
-            const int awF = (P.off + ah + 1) >> 2, aoF = (P.off + ah + 1) & 3;
-            const int awB = (P.off + ah - 4) >> 2, aoB = (P.off + ah) & 3;
-            const uint32_t asF =
-                (uint32_t)(aoF | ((aoF + 1) << 4) | ((aoF + 2) << 8) | ((aoF + 3) << 12));
-            const uint32_t asB =
-                (uint32_t)((aoB + 3) | ((aoB + 2) << 4) | ((aoB + 1) << 8) | (aoB << 12));
+            const uint32_t* Xa = apar ? w.X1w : w.X0w;
+            const int awF = (P.xoff + ah + 1) >> 2;
+            const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
+            const int awB = (P.xoff + ah - 4) >> 2;
+            const uint32_t asB = sel4r((P.xoff + ah) & 3);
             const int tstar = cen ? -1 : (k - astar);
             const int mul = cen ? -2 * xa : -4 * xa;
-            int csp = 0, cmx = 0, esp = 0;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int s = lane + 32 * jj;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) cn[jj][b] = 0;
                 if (jj < nj && s < S) {
-                    const uint32_t y = prmt(Fa[awF + s], Fa[awF + s + 1], asF) +
-                                       prmt(Fa[awB - s], Fa[awB - s + 1], asB);
+                    const uint32_t cw0 = w.C16[2 * s], cw1 = w.C16[2 * s + 1];
+                    const uint32_t fw = prmt(Xa[awF + s], Xa[awF + s + 1], asF);
+                    const uint32_t bw = prmt(Xa[awB - s], Xa[awB - s + 1], asB);
+                    cn[jj][0] = (int)(int16_t)(cw0 & 0xffff);
+                    cn[jj][1] = (int)(int16_t)(cw0 >> 16);
+                    cn[jj][2] = (int)(int16_t)(cw1 & 0xffff);
+                    cn[jj][3] = (int)(int16_t)(cw1 >> 16);
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
                         const int t = 4 * s + 1 + b;
-                        int v = (int)((y >> (8 * b)) & 0xFF) - 2;
+                        int v = sbyte(fw, b) + sbyte(bw, b);
                         if (t == tstar) v -= xb;
-                        if (t <= k) c[jj][b] += mul * v;
-                        csp += c[jj][b];
-                        cmx = max(cmx, abs(c[jj][b]));
-                        esp += c[jj][b] * c[jj][b];
+                        cn[jj][b] += mul * v;
+                        cmx = max(cmx, abs(cn[jj][b]));
+                        if (P.debug_check) esp += cn[jj][b] * cn[jj][b];
                     }
                 }
             }
-            // incremental Q: flip astar, then bstar (sequential single flips)
-            if (par == apar) {
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    const int a = a0 + 8 * m;
-                    if (a > k) continue;
-                    const int lim = L - 1 - a;  // b(a)
-                    // flip 1: j = astar, old value xa
-                    if (a != astar) {
-                        const int jp = 2 * a - astar;
-                        if (jp >= 0 && jp <= L - 1 && !(a < k && max(astar, jp) == lim))
-                            q[m] -= 2 * xa * (ybyte(w, P, jp) - 1);
-                    }
-                    // flip 2: j = bstar, old value xb, after astar flipped
-                    if (!cen && a != bstar) {
-                        const int jp = 2 * a - bstar;
-                        if (jp >= 0 && jp <= L - 1 && !(a < k && max(bstar, jp) == lim)) {
-                            const int xjp = (jp == astar) ? -xa : (ybyte(w, P, jp) - 1);
-                            q[m] -= 2 * xb * xjp;
+            // incremental 16N+32Q: neighbours of astar's parity (lanes over a)
+            const int alo = P.p + ((P.p ^ apar) & 1);
+            for (int a = alo + 2 * lane; a <= k; a += 64) {
+                const int lim = L - 1 - a;
+                int dq = 0;
+                if (a != astar) {
+                    const int jp = 2 * a - astar;
+                    if (jp >= 0 && !(a < k && max(astar, jp) == lim)) dq -= xa * xval(w, P, jp);
+                    if (!cen) {
+                        const int jq = 2 * a - bstar;
+                        if (jq >= 0 && !(a < k && bstar == lim)) {
+                            const int xq = (jq == astar) ? -xa : xval(w, P, jq);
+                            dq -= xb * xq;
                         }
                     }
                 }
+                if (dq) w.KQ[a] += (a < k ? 64 : 16) * dq;
             }
-            __syncwarp();
+        }
+        const bool wide_next = __reduce_max_sync(FULLMASK, (unsigned)cmx) > 127u;  // also syncs
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int s = lane + 32 * jj;
-                if (jj < nj && s < S) {
-                    const uint32_t p01 = prmt((uint32_t)c[jj][0], (uint32_t)c[jj][1], 0x0040);
-                    const uint32_t p23 = prmt((uint32_t)c[jj][2], (uint32_t)c[jj][3], 0x0040);
-                    w.C8[s] = prmt(p01, p23, 0x5410);
-                    w.C16[2 * s] = prmt((uint32_t)c[jj][0], (uint32_t)c[jj][1], 0x5410);
-                    w.C16[2 * s + 1] = prmt((uint32_t)c[jj][2], (uint32_t)c[jj][3], 0x5410);
-                }
-            }
-            if (lane == 0) w.Fb[apar * P.nwp * 4 + P.off + ah] = (uint8_t)(1 - xa);
-            if (lane == 1 && !cen)
-                w.Fb[(bstar & 1) * P.nwp * 4 + P.off + (bstar >> 1)] = (uint8_t)(1 - xb);
-            if (lane == 2) w.half[astar >> 5] ^= 1u << (astar & 31);
-            csum = warp_sum(csp);
-            wide = __reduce_max_sync(FULLMASK, (unsigned)cmx) > 127u;
-            if (P.debug_check) {
-                const int echk = warp_sum(esp);
-                if (echk != energy + dstar) ++diverged;
-            }
+        for (int jj = 0; jj < 4; ++jj) {
+            const int up = __shfl_up_sync(FULLMASK, cn[jj][3], 1);
+            const int wrap = __shfl_sync(FULLMASK, jj > 0 ? cn[jj > 0 ? jj - 1 : 0][3] : 0, 31);
+            const int s = lane + 32 * jj;
+            const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
+            if (jj < nj && s < S) store_c_word(w, P, s, cn[jj], cprev, wide_next);
+        }
+        wide = wide_next;
+        if (lane == 0) ((astar & 1) ? w.X1 : w.X0)[P.xoff + (astar >> 1)] = (int8_t)(-xa);
+        if (lane == 1 && !cen) ((bstar & 1) ? w.X1 : w.X0)[P.xoff + (bstar >> 1)] = (int8_t)(-xb);
+        if (lane == 2) w.half[astar >> 5] ^= 1u << (astar & 31);
+        if (P.debug_check) {
+            const int echk = warp_sum(esp);
+            if (echk != energy + dstar) ++diverged;
         }
         h1 ^= fm0[astar];
         h2 ^= fm1[astar];
@@ -528,12 +537,12 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     __syncwarp();
 }
 
-template <int R, bool COUNT>
 #ifndef LABS_MIN_BLOCKS
-#define LABS_MIN_BLOCKS 4
+#define LABS_MIN_BLOCKS 6
 #endif
+template <int R, bool COUNT>
 __global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkParams P, int* score_out,
-                                                       int* corr_out) {
+                                                                        int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
     for (int i = threadIdx.x; i < 2 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
@@ -542,10 +551,14 @@ __global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkPara
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + fm_words + warp * P.warp_words;
     WarpSmem w;
-    w.F = base;
-    w.Fb = reinterpret_cast<uint8_t*>(base);
-    w.C8 = base + P.off_c8;
+    w.X0w = base;
+    w.X1w = base + P.off_x1;
+    w.X0 = reinterpret_cast<int8_t*>(w.X0w);
+    w.X1 = reinterpret_cast<int8_t*>(w.X1w);
+    w.KL = base + P.off_kl;
+    w.KH = base + P.off_kh;
     w.C16 = base + P.off_c16;
+    w.KQ = reinterpret_cast<int*>(base + P.off_kq);
     w.half = base + P.off_half;
     w.bloom = base + P.off_bloom;
     const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
