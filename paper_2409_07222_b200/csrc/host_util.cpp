@@ -145,7 +145,8 @@ std::string derive(const labs_saw_config& cfg, Derived& d) {
         return "saw: no stop condition configured";
     if (cfg.bloom_fpr <= 0 || cfg.bloom_fpr >= 1) return "BloomFilter: fpr must be in (0,1)";
     if (d.p > 30) return "rank_prefixes: p > 30 is not enumerable";
-    if (d.kp1 > kMaxHalf) return "saw: length exceeds the tabulation hash range (k+1 <= 1024)";
+    if (L > kMaxHalf)  // canonical_hash(0) of the full sequence indexes t_[0][i < L] (rng.hpp:77,89-95)
+        return "saw: length exceeds the tabulation hash range (L <= 1023)";
     bloom_size(static_cast<uint64_t>(d.t_i) + 1, cfg.bloom_fpr, d.bloom_bits, d.bloom_k);
     if (d.p == 0) {
         d.nprefix = 1;

@@ -1,0 +1,105 @@
+"""N>1 host path on CPU: class sharding + gather + merge over torch.distributed (gloo).
+
+The per-rank GPU call is replaced by the CPU oracle run on the same shard config (the
+`runner` seam of run_saw_pool_distributed), so this covers exactly the multi-process
+logic bench.py / a torchrun job uses, at world_size 2 and 3, against the single-process
+pool of the reference semantics (--threads 1 order, DedupSink).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.oracle import make_config
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_runner(scfg):
+    from oracle.oracle import Restated
+    from paper_2409_07222_b200.api import Candidate, PoolStats
+
+    run = Restated().run_saw_pool(make_config(
+        scfg.length, walkers=scfg.walkers, prefix_len=scfg.prefix_len,
+        target_merit=scfg.target_merit, energy_threshold=scfg.energy_threshold,
+        max_restarts=scfg.max_restarts, seed=scfg.seed, shard_index=scfg.shard_index,
+        shard_count=scfg.shard_count))
+    cands = [Candidate(c.seq, c.energy, "saw", np.zeros(0, np.int8), c.walker, c.restart,
+                       c.iteration) for c in run.candidates]
+    st = PoolStats(walks=run.stats["walks"], iterations=run.stats["iterations"],
+                   emitted=run.stats["emitted"], best_energy=run.stats["best_energy"],
+                   delta_evals=run.stats["delta_evals"])
+    return cands, st
+
+
+CFG = dict(length=51, walkers=24, prefix_len=4, max_restarts=2, target_merit=3.6, seed=8)
+
+
+def _worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_07222_b200 import CollectingSink, SawConfig
+        from paper_2409_07222_b200.distributed import run_saw_pool_distributed
+
+        sink = CollectingSink()
+        st = run_saw_pool_distributed(SawConfig(**CFG), sink, runner=_oracle_runner)
+        if rank == 0:
+            got = sink.take()
+            np.savez(out_path, seq=np.array([c.seq for c in got]),
+                     e=np.array([c.energy for c in got]),
+                     key=np.array([(c.walker, c.restart, c.iteration) for c in got]),
+                     stats=np.array([st.walks, st.iterations, st.emitted, st.best_energy,
+                                     st.delta_evals]))
+        else:
+            assert st is None
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_shard_merge_equals_single_pool(tmp_path, restated, world):
+    out = str(tmp_path / "merged.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world,
+                       start_method="spawn", join=True)
+    got = np.load(out)
+    ref = restated.run_saw_pool(make_config(**CFG))
+    assert len(got["e"]) == len(ref.candidates) > 0
+    assert [tuple(k) for k in got["key"]] == [(c.walker, c.restart, c.iteration)
+                                              for c in ref.candidates]
+    assert list(got["e"]) == [c.energy for c in ref.candidates]
+    assert all(np.array_equal(a, c.seq) for a, c in zip(got["seq"], ref.candidates))
+    assert list(got["stats"]) == [ref.stats["walks"], ref.stats["iterations"],
+                                  ref.stats["emitted"], ref.stats["best_energy"],
+                                  ref.stats["delta_evals"]]
+
+
+def test_merge_dedups_across_shards():
+    from paper_2409_07222_b200.api import Candidate
+    from paper_2409_07222_b200.distributed import merge_shards
+
+    s = np.array([1, -1, 1], np.int8)
+    t = np.array([1, 1, -1], np.int8)
+    a = [Candidate(s, 1, walker=2, restart=0, iteration=5)]
+    b = [Candidate(s, 1, walker=1, restart=3, iteration=9), Candidate(t, 2, walker=1, restart=4,
+                                                                      iteration=1)]
+    m = merge_shards([a, b])
+    assert [(c.walker, c.restart) for c in m] == [(1, 3), (1, 4)]
+
+
+def test_shard_config_rejects_coupled_modes():
+    from paper_2409_07222_b200 import SawConfig
+    from paper_2409_07222_b200.distributed import shard_config
+
+    with pytest.raises(ValueError):
+        shard_config(SawConfig(length=51, target_merit=3.0, candidate_quota=5), 0, 2)
+    c = shard_config(SawConfig(length=51, target_merit=3.0), 1, 2)
+    assert (c.shard_index, c.shard_count) == (1, 2)
