@@ -92,6 +92,8 @@ typedef struct labs_pool_stats {
     double seed_ms;            /* device time of the seed kernels */
     int32_t n_gpus;
     int32_t _pad;
+    int64_t h2d_bytes;         /* host->device bytes copied by this call */
+    int64_t d2h_bytes;         /* device->host bytes copied by this call */
 } labs_pool_stats;
 
 /* Replaces run_saw_pool (saw.cpp:218-267).  Candidates reach `emit` deduplicated
@@ -152,14 +154,17 @@ int labs_enumerate_class(int32_t length, int32_t prefix_len, int32_t class_index
                          labs_enum_fn emit, void* user, labs_enum_stats* stats);
 
 /* Device-resident benchmark plan: the whole pool's walks with inputs in HBM.
- * labs_bench_run times `reps` launches (seed + walk kernels) with CUDA events. */
+ * labs_bench_run times `reps` launches (seed + walk kernels) with CUDA events on the
+ * library's stream; before every rep (outside the timed events) a 256 MiB scratch
+ * buffer is written so that no rep starts with a warm L2. */
 typedef struct labs_bench_plan labs_bench_plan;
 int labs_bench_create(const labs_saw_config* cfg, labs_bench_plan** out);
 int labs_bench_run(labs_bench_plan* plan, int32_t reps, double* ms_per_rep,
                    labs_pool_stats* last);
 void labs_bench_destroy(labs_bench_plan* plan);
 
-/* INT32 issue-rate microbenchmark: ops/s of IMAD-only, IADD3/LOP3-only and a 1:1 mix. */
+/* INT32 issue-rate microbenchmark (all SMs, CUDA events): lane-ops/s of IMAD-only,
+ * IADD3/LOP3/SHF-only and a 1:1 mix, and IDP4A lane-instructions/s (each = 4 int8 MACs). */
 int labs_int32_peak(double* imad_ops, double* ialu_ops, double* mixed_ops, double* dp4a_ops,
                     int32_t* sm_count, int32_t* clock_khz);
 

@@ -289,6 +289,7 @@ class Reference(_Base):
         L.ref_last_error.restype = C.c_char_p
         L.ref_run_saw_pool.argtypes = [C.POINTER(SawConfigC), C.c_int, CAND_FN, C.c_void_p,
                                        C.POINTER(PoolStatsC)]
+        L.ref_count_deltas.argtypes = [C.POINTER(SawConfigC), C.c_int, C.POINTER(PoolStatsC)]
         L.ref_walk_trace.argtypes = [C.POINTER(SawConfigC), CAND_FN, WALK_FN, C.c_void_p,
                                      C.POINTER(PoolStatsC)]
         for name in ("ref_skew_flip_delta_fast", "ref_skew_flip_delta"):
@@ -333,6 +334,13 @@ class Reference(_Base):
             raise ValueError(self.lib.ref_last_error().decode())
         run.stats = _stats(st)
         return run
+
+    def count_deltas(self, cfg: SawConfigC, threads: int = 1) -> dict:
+        """skew_flip_delta_fast calls + iterations of the pool's walks (threaded, no sink)."""
+        st = PoolStatsC()
+        if self.lib.ref_count_deltas(C.byref(cfg), threads, C.byref(st)) != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return _stats(st)
 
     def skew_flip_delta_fast(self, s, hp):
         a, p = _i8(s)

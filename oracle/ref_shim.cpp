@@ -6,8 +6,11 @@
 // the C restatement (labs_oracle.c) and the CUDA path against the real thing,
 // and so that bench.py --impl reference can time the unmodified reference.
 #include <cstring>
+#include <atomic>
 #include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "labs/candidate.hpp"
 #include "labs/hex_codec.hpp"
@@ -147,6 +150,57 @@ int ref_walk_trace(const lo_saw_config* cfg, lo_candidate_fn cand, lo_walk_fn wa
             }
         }
         if (out) *out = st;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Counting-only, multi-threaded walker_loop replica: the number of
+// skew_flip_delta_fast calls (unvisited free neighbours, saw.cpp:109-113) and
+// iterations of the pool's walks, with `threads` std::threads striding walkers
+// like run_saw_pool (saw.cpp:242-257).  Used to size the CPU baseline sample.
+int ref_count_deltas(const lo_saw_config* cfg, int threads, lo_pool_stats* out) {
+    try {
+        SawConfig sc = to_saw(cfg, 1);
+        sc.validate();
+        const int p = sc.effective_prefix_len();
+        std::vector<PartitionPrefix> prefixes;
+        if (p == 0) prefixes.push_back(PartitionPrefix{{}, 0});
+        else prefixes = rank_prefixes(p);
+        const int w0 = cfg->walker_begin > 0 ? cfg->walker_begin : 0;
+        const int w1 = cfg->walker_end > 0 && cfg->walker_end < sc.walkers ? cfg->walker_end
+                                                                            : sc.walkers;
+        std::atomic<long long> walks{0}, iters{0}, deltas{0};
+        std::atomic<int> next{w0};
+        auto job = [&]() {
+            class NullSink final : public CandidateSink {
+            public:
+                void emit(const Candidate&) override {}
+            } sink;
+            for (int w = next++; w < w1; w = next++) {
+                const std::size_t cls = static_cast<std::size_t>(w) % prefixes.size();
+                Rng rng(sc.seed, static_cast<std::uint64_t>(w));
+                CountingVisited visited(static_cast<std::size_t>(sc.effective_iterations()) + 1,
+                                        sc.bloom_fpr);
+                for (long long r = 0; r < sc.max_restarts; ++r) {
+                    const WalkStats ws = run_walk(sc, prefixes[cls], rng, visited, sink);
+                    ++walks;
+                    iters += ws.iterations;
+                }
+                deltas += visited.misses;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 0; t < (threads > 0 ? threads : 1); ++t) th.emplace_back(job);
+        for (auto& t : th) t.join();
+        if (out) {
+            std::memset(out, 0, sizeof *out);
+            out->walks = walks;
+            out->iterations = iters;
+            out->delta_evals = deltas;
+        }
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

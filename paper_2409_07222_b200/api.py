@@ -71,7 +71,7 @@ class _PoolStats(C.Structure):
         ("delta_evals", C.c_int64), ("delta_evals_computed", C.c_int64),
         ("exhausted_walks", C.c_int64), ("wide_iterations", C.c_int64),
         ("kernel_ms", C.c_double), ("seed_ms", C.c_double), ("n_gpus", C.c_int32),
-        ("_pad", C.c_int32),
+        ("_pad", C.c_int32), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
     ]
 
 
@@ -299,6 +299,8 @@ class PoolStats:
     kernel_ms: float = 0.0
     seed_ms: float = 0.0
     n_gpus: int = 1
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
     @classmethod
     def _from(cls, s: _PoolStats) -> "PoolStats":

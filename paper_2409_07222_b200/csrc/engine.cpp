@@ -85,6 +85,7 @@ struct BatchOut {
     std::vector<int64_t> stats;   // nwalks x kWalkStatWords
     std::vector<int64_t> walk_walker, walk_restart;  // per batch walk
     double kernel_ms = 0, seed_ms = 0;
+    int64_t h2d = 0, d2h = 0;  // bytes copied for this batch
 };
 
 // Per-device state: stream, events, uploaded tables, batch buffers.
@@ -172,6 +173,7 @@ public:
         LABS_CUDA(cudaMemcpyAsync(seg_init.p, init.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
         LABS_CUDA(cudaMemcpyAsync(rng.p, hs.data(), 32 * static_cast<size_t>(nseg),
                                   cudaMemcpyHostToDevice, st));
+        out.h2d += static_cast<int64_t>(nseg) * (4 + 4 + 8 + 8 + 4 + 32);
         SeedParams sp{};
         sp.kp1 = wp.kp1;
         sp.p = wp.p;
@@ -191,6 +193,7 @@ public:
         LABS_CUDA(cudaMemcpyAsync(hs.data(), rng.p, 32 * static_cast<size_t>(nseg),
                                   cudaMemcpyDeviceToHost, st));
         LABS_CUDA(cudaStreamSynchronize(st));
+        out.d2h += 32 * static_cast<int64_t>(nseg);
         float ms = 0;
         LABS_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
         out.seed_ms += ms;
@@ -244,6 +247,7 @@ public:
             LABS_CUDA(cudaMemcpyAsync(out.stats.data(), stats.p, out.stats.size() * 8,
                                       cudaMemcpyDeviceToHost, st));
             LABS_CUDA(cudaStreamSynchronize(st));
+            out.d2h += static_cast<int64_t>(sizeof cnt + out.rec.size() * 4 + out.stats.size() * 8);
             return;
         }
         throw CudaFailure("record buffer overflow persisted");
@@ -500,6 +504,8 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
                 for (const auto& b : outs[static_cast<size_t>(g)]) {
                     kms += b.kernel_ms;
                     sms += b.seed_ms;
+                    acc.st.h2d_bytes += b.h2d;
+                    acc.st.d2h_bytes += b.d2h;
                 }
                 acc.st.kernel_ms = std::max(acc.st.kernel_ms, kms);
                 acc.st.seed_ms = std::max(acc.st.seed_ms, sms);
@@ -590,6 +596,8 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
                 dr.walk(nw, b);
                 acc.st.kernel_ms += b.kernel_ms;
                 acc.st.seed_ms += b.seed_ms;
+                acc.st.h2d_bytes += b.h2d;
+                acc.st.d2h_bytes += b.d2h;
                 process_batch(segs, b);
                 wi = wj;
                 next_r = r;
@@ -721,6 +729,8 @@ struct BenchPlan {
     labs_saw_config cfg;
     Derived d;
     std::unique_ptr<DeviceRunner> dr;
+    DevBuf<uint8_t> l2_scratch;  // written before every rep: no rep starts with a warm L2
+    static constexpr size_t kL2Flush = size_t(256) << 20;
     std::vector<Segment> segs;
     int64_t nwalks = 0;
 };
@@ -876,7 +886,9 @@ int labs_bench_run(labs_bench_plan* plan, int32_t reps, double* ms_per_rep, labs
         LABS_CUDA(cudaSetDevice(dr.dev));
         double total = 0;
         BatchOut b;
+        bp.l2_scratch.reserve(BenchPlan::kL2Flush);
         for (int r = 0; r < reps; ++r) {
+            LABS_CUDA(cudaMemsetAsync(bp.l2_scratch.p, r & 0xff, BenchPlan::kL2Flush, dr.st));
             b = BatchOut();
             std::vector<std::array<uint64_t, 4>> states(bp.segs.size());
             std::vector<int32_t> init(bp.segs.size(), 1);

@@ -1,9 +1,442 @@
-// enum_kernels.cu -- K4 restriction-class Gray enumeration (placeholder, replaced below)
+// enum_kernels.cu -- K4: restriction-class Gray enumeration on sm_100a (extension;
+// BASELINE config 2).
+//
+// The reference has no Step-1 enumeration mode; the pattern is oracle_skew_exhaustive
+// (oracle.cpp:37-67): start from a half, visit configurations in Gray order, each step
+// one apply_skew_flip (skew.cpp:95-105) at half position p + ctz(g), test E.  Here the
+// half is rank_prefixes(p)[class] ++ (+1)^(k+1-p) and the Gray code runs over the m
+// half positions [p, p+m); configuration g = Gray(g) (bit j set <=> position p+j is -1).
+// Every g in [g_begin, g_end) with E < E_l is emitted; best E and its first g reported.
+//
+// Layout: one warp = one chunk of 2^chunk_log2 consecutive g (grid-stride over chunks).
+// Lanes own the even lags t = 4(lane + 32j) + 1 .. +4 (C_{2t} in registers); the
+// sequence lives in shared memory as two parity byte arrays.  A step's energy change
+//     dE = sum_t dc_t (2 C_{2t} + dc_t),   dc_t = mul * (x_{a+2t} + x_{a-2t} - [t = k-a] x_b)
+// (mul = -4 x_a, or -2 x_a for the centre; the same fused even-lag rule as the walk
+// kernel's apply) is accumulated per lane for 32 steps in registers and then reduced
+// with one 31-shuffle transpose-reduction + a lane scan, so each lane ends up holding
+// the energy of one configuration: the warp-wide reduction costs ~4 instructions per
+// step instead of 10.  Exact integer arithmetic throughout.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <chrono>
 #include <string>
-#include "../../include/labs_gpu.h"
-namespace labs_b200 { void set_error(const std::string& msg); }
-extern "C" int labs_enumerate_class(int32_t, int32_t, int32_t, int32_t, int64_t, uint64_t, uint64_t,
-                                    labs_enum_fn, void*, labs_enum_stats*) {
-    labs_b200::set_error("enumeration not built");
-    return LABS_EINVAL;
+#include <vector>
+
+#include "host_util.hpp"
+
+namespace labs_b200 {
+
+#define FULLMASK 0xffffffffu
+
+struct EnumLaunch {
+    int32_t L, k, kp1, p, m;
+    int32_t nj;            // lag groups per lane (t = 4(lane + 32j) + 1..4)
+    int32_t S;             // 4-lag words covering t = 1..k
+    int32_t xoff, xwords;  // parity arrays: byte xoff + i = x_{2i+par}, zero padded
+    int32_t nwx;           // words per parity array holding data
+    int32_t warp_words;
+    int32_t chunk_log2;
+    int64_t e_l;
+    uint64_t g_begin, g_end;
+    uint64_t nchunks;
+    uint32_t base_half[kMaxHalf / 32];  // half of configuration 0 (bit set <=> +1)
+    uint32_t* rec;                      // [rec_cap][4]: g lo, g hi, E, 0
+    int64_t rec_cap;
+    unsigned long long* rec_count;
+    int64_t* chunk_best;                // [nchunks][2]: best E, its first g
+};
+
+__device__ __forceinline__ uint32_t sel4(int o) {
+    return (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+}
+__device__ __forceinline__ uint32_t sel4r(int o) {
+    return (uint32_t)((o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
+}
+__device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
+
+template <int NJ>
+__device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t chunk, int lane) {
+    const int L = P.L, k = P.k;
+    const uint64_t g0 = P.g_begin + (chunk << P.chunk_log2);
+    uint64_t g1 = g0 + (1ull << P.chunk_log2);
+    if (g1 > P.g_end || g1 < g0) g1 = P.g_end;
+    uint32_t* X0w = reinterpret_cast<uint32_t*>(X0);
+    uint32_t* X1w = reinterpret_cast<uint32_t*>(X1);
+
+    // ---- configuration g0: half = base with Gray(g0) over [p, p+m) negated ----
+    const uint64_t gray0 = g0 ^ (g0 >> 1);
+    for (int wi = lane; wi < 2 * P.xwords; wi += 32) {
+        const int par = wi >= P.xwords;
+        const int word = wi - par * P.xwords;
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int li = word * 4 + b - P.xoff;
+            const int j = 2 * li + par;
+            int x = 0;
+            if (li >= 0 && j < L) {
+                int src = j, neg = 0;
+                if (j > k) {
+                    src = 2 * k - j;
+                    neg = (j - k) & 1;
+                }
+                int bit = (P.base_half[src >> 5] >> (src & 31)) & 1;
+                if (src >= P.p && src < P.p + P.m && ((gray0 >> (src - P.p)) & 1)) bit ^= 1;
+                x = (bit ^ neg) ? 1 : -1;
+            }
+            v |= ((uint32_t)x & 0xffu) << (8 * b);
+        }
+        (par ? X1w : X0w)[word] = v;
+    }
+    __syncwarp();
+
+    // ---- C_{2t} of the owned lags (sequence.cpp:8-19 on the parity arrays) ----
+    int C[NJ][4];
+    int e_part = 0;
+    const int n0 = P.xoff >> 2;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int t = 4 * (lane + 32 * j) + 1 + b;
+            int acc = 0;
+            if (t <= k) {
+                const int dw = t >> 2;
+                const uint32_t sel = sel4(t & 3);
+                for (int n = n0; n < n0 + P.nwx; ++n) {
+                    acc = __dp4a((int)X0w[n], (int)__byte_perm(X0w[n + dw], X0w[n + dw + 1], sel), acc);
+                    acc = __dp4a((int)X1w[n], (int)__byte_perm(X1w[n + dw], X1w[n + dw + 1], sel), acc);
+                }
+            }
+            C[j][b] = acc;
+            e_part += acc * acc;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e_part += __shfl_xor_sync(FULLMASK, e_part, o);
+    int energy = e_part;
+
+    int best_e = energy;
+    uint64_t best_g = g0;
+    if (energy < P.e_l && lane == 0) {
+        const unsigned long long slot = atomicAdd(P.rec_count, 1ull);
+        if ((long long)slot < P.rec_cap) {
+            uint32_t* r = P.rec + 4 * slot;
+            r[0] = (uint32_t)g0;
+            r[1] = (uint32_t)(g0 >> 32);
+            r[2] = (uint32_t)energy;
+            r[3] = 0;
+        }
+    }
+
+    // ---- Gray steps g = g0+1 .. g1-1 in batches of 32 ----
+    const uint64_t nsteps = g1 - g0 - 1;
+    for (uint64_t s0 = 0; s0 < nsteps; s0 += 32) {
+        int part[32];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+            part[s] = 0;
+            if (s0 + s < nsteps) {  // warp-uniform
+                const uint64_t g = g0 + 1 + s0 + s;
+                const int a = P.p + (__ffsll((long long)g) - 1);
+                const int ah = a >> 1;
+                int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
+                const uint32_t* Xaw = (a & 1) ? X1w : X0w;
+                const int xa = Xa[ah];
+                const bool cen = a == k;
+                const int tstar = cen ? -1 : k - a;
+                const int xb = ((k - a) & 1) ? -xa : xa;
+                const int mul = cen ? -2 * xa : -4 * xa;
+                const int awF = (P.xoff + ah + 1) >> 2;
+                const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
+                const int awB = (P.xoff + ah - 4) >> 2;
+                const uint32_t asB = sel4r((P.xoff + ah) & 3);
+                int acc = 0;
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const int sw = lane + 32 * j;
+                    if (sw < P.S) {  // lanes past the lag range read nothing
+                        const uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
+                        const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int t = 4 * sw + 1 + b;
+                            int v = sbyte(fw, b) + sbyte(bw, b);
+                            if (t == tstar) v -= xb;
+                            const int dc = mul * v;  // 0 for t > k (zero padding)
+                            acc += dc * (2 * C[j][b] + dc);
+                            C[j][b] += dc;
+                        }
+                    }
+                }
+                part[s] = acc;
+                __syncwarp();
+                if (lane == 0) Xa[ah] = (int8_t)(-xa);
+                if (lane == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
+                __syncwarp();
+            }
+        }
+        // transpose-reduce: lane l ends with sum over lanes of part[l]
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const bool up = lane & off;
+#pragma unroll
+            for (int i = 0; i < off; ++i) {
+                const int send = up ? part[i] : part[i + off];
+                const int keep = up ? part[i + off] : part[i];
+                part[i] = keep + __shfl_xor_sync(FULLMASK, send, off);
+            }
+        }
+        int e = part[0];  // dE of step s0 + lane
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLMASK, e, o);
+            if (lane >= o) e += y;
+        }
+        const bool valid = s0 + lane < nsteps;
+        const int e_mine = energy + e;
+        const uint64_t g_mine = g0 + 1 + s0 + lane;
+        energy = __shfl_sync(FULLMASK, e_mine, 31);  // all 32 steps valid unless last batch
+        if (s0 + 32 > nsteps) energy = __shfl_sync(FULLMASK, e_mine, (int)(nsteps - s0 - 1));
+        if (valid && e_mine < best_e) {
+            best_e = e_mine;
+            best_g = g_mine;
+        }
+        const bool hit = valid && e_mine < P.e_l;
+        const unsigned hm = __ballot_sync(FULLMASK, hit);
+        if (hm) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(P.rec_count, (unsigned long long)__popc(hm));
+            base = __shfl_sync(FULLMASK, base, 0);
+            if (hit) {
+                const unsigned long long slot = base + __popc(hm & ((1u << lane) - 1));
+                if ((long long)slot < P.rec_cap) {
+                    uint32_t* r = P.rec + 4 * slot;
+                    r[0] = (uint32_t)g_mine;
+                    r[1] = (uint32_t)(g_mine >> 32);
+                    r[2] = (uint32_t)e_mine;
+                    r[3] = 0;
+                }
+            }
+        }
+    }
+    // chunk best: lowest E, then lowest g
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int oe = __shfl_xor_sync(FULLMASK, best_e, o);
+        const unsigned long long og = __shfl_xor_sync(FULLMASK, (unsigned long long)best_g, o);
+        if (oe < best_e || (oe == best_e && og < best_g)) {
+            best_e = oe;
+            best_g = og;
+        }
+    }
+    if (lane == 0) {
+        P.chunk_best[2 * chunk] = best_e;
+        P.chunk_best[2 * chunk + 1] = (int64_t)best_g;
+    }
+    __syncwarp();
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P) {
+    extern __shared__ uint32_t esmem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int8_t* X0 = reinterpret_cast<int8_t*>(esmem + warp * P.warp_words);
+    int8_t* X1 = X0 + 4 * P.xwords;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t c = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < P.nchunks; c += nwarps)
+        enum_chunk<NJ>(P, X0, X1, c, lane);
+}
+
+namespace {
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+};
+#define ENUM_CUDA(call)                                                       \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) {                                              \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+            return LABS_ECUDA;                                                \
+        }                                                                     \
+    } while (0)
+}  // namespace
+
+int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_l,
+                        uint64_t g_begin, uint64_t g_end, labs_enum_fn emit, void* user,
+                        labs_enum_stats* stats, int chunk_log2) {
+    const int kp1 = (L + 1) / 2;
+    if (L < 3 || L % 2 == 0) {
+        set_error("enumerate: length must be odd and >= 3");
+        return LABS_EINVAL;
+    }
+    if (L > kMaxHalf) {
+        set_error("enumerate: length exceeds the tabulation hash range (L <= 1023)");
+        return LABS_EINVAL;
+    }
+    if (p < 1 || p > kp1 || p > 30) {
+        set_error("enumerate: bad prefix length");
+        return LABS_EINVAL;
+    }
+    if (m < 0 || p + m > kp1 || m > 62) {
+        set_error("enumerate: bad free-bit count");
+        return LABS_EINVAL;
+    }
+    if (cls < 0 || cls >= (1 << (p - 1))) {
+        set_error("enumerate: bad class");
+        return LABS_EINVAL;
+    }
+    const uint64_t total = 1ull << m;
+    if (g_end > total) g_end = total;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+        set_error("no CUDA device available (the enumeration has no CPU fallback)");
+        return LABS_ENODEV;
+    }
+    labs_enum_stats st{};
+    st.best_energy = 0;
+    if (g_begin >= g_end) {
+        if (stats) *stats = st;
+        return LABS_OK;
+    }
+    EnumLaunch P{};
+    P.L = L;
+    P.k = (L - 1) / 2;
+    P.kp1 = kp1;
+    P.p = p;
+    P.m = m;
+    P.nj = (P.k + 127) / 128;
+    P.nwx = (kp1 + 3) / 4;
+    // window reads reach S+1 words past any position on both sides (lanes with 4-lag
+    // word sw < S only); the correlation prologue reads up to nwx + S + 1 words
+    const int S = (P.k + 3) / 4;
+    P.S = S;
+    P.xoff = 4 * S + 16;
+    P.xwords = ((P.xoff + 4 * P.nwx + 4 * S + 32) / 4 + 3) & ~3;
+    P.warp_words = 2 * P.xwords;
+    const uint64_t range = g_end - g_begin;
+    int cl = chunk_log2 > 0 ? chunk_log2 : 12;
+    while (cl > 5 && (range >> cl) < 148ull * 32) --cl;  // enough chunks to fill the GPU
+    P.chunk_log2 = cl;
+    P.nchunks = (range + (1ull << cl) - 1) >> cl;
+    P.e_l = e_l;
+    P.g_begin = g_begin;
+    P.g_end = g_end;
+    const auto pre = rank_prefixes(p);
+    for (int i = 0; i < kp1; ++i) {
+        const bool plus = i < p ? pre[static_cast<size_t>(cls) * p + i] > 0 : true;
+        if (plus) P.base_half[i >> 5] |= 1u << (i & 31);
+    }
+    cudaStream_t stream;
+    ENUM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    DBuf<uint32_t> rec;
+    DBuf<unsigned long long> cnt;
+    DBuf<int64_t> best;
+    int64_t cap = 1 << 16;
+    int rc = LABS_OK;
+    std::vector<uint32_t> hrec;
+    std::vector<int64_t> hbest(2 * P.nchunks);
+    unsigned long long hcnt = 0;
+    float ms_total = 0;
+    do {
+        cudaError_t ce = cudaSuccess;
+        if (!cnt.p) ce = cudaMalloc(&cnt.p, sizeof(unsigned long long));
+        if (ce == cudaSuccess && !best.p) ce = cudaMalloc(&best.p, 16 * P.nchunks);
+        if (ce == cudaSuccess) {
+            if (rec.p) cudaFree(rec.p);
+            rec.p = nullptr;
+            ce = cudaMalloc(&rec.p, 16 * static_cast<size_t>(cap));
+        }
+        if (ce != cudaSuccess) {
+            set_error(std::string("enumerate: ") + cudaGetErrorString(ce));
+            rc = LABS_ECUDA;
+            break;
+        }
+        P.rec = rec.p;
+        P.rec_cap = cap;
+        P.rec_count = cnt.p;
+        P.chunk_best = best.p;
+        cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), stream);
+        const size_t smem = static_cast<size_t>(4) * P.warp_words * 4;
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const uint64_t want = (P.nchunks + 3) / 4;
+        const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sms) * 8));
+        cudaEventRecord(e0, stream);
+        switch (P.nj) {
+            case 1: enum_kernel<1><<<grid, 128, smem, stream>>>(P); break;
+            case 2: enum_kernel<2><<<grid, 128, smem, stream>>>(P); break;
+            case 3: enum_kernel<3><<<grid, 128, smem, stream>>>(P); break;
+            default: enum_kernel<4><<<grid, 128, smem, stream>>>(P); break;
+        }
+        cudaEventRecord(e1, stream);
+        ce = cudaGetLastError();
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hcnt, cnt.p, sizeof hcnt, cudaMemcpyDeviceToHost, stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(stream);
+        if (ce != cudaSuccess) {
+            set_error(std::string("enumerate kernel: ") + cudaGetErrorString(ce));
+            rc = LABS_ECUDA;
+            break;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms_total += ms;
+        if (static_cast<int64_t>(hcnt) > cap) {  // overflow: grow and rerun (deterministic)
+            cap = static_cast<int64_t>(hcnt) + 1024;
+            continue;
+        }
+        hrec.resize(4 * static_cast<size_t>(hcnt));
+        if (hcnt) cudaMemcpy(hrec.data(), rec.p, hrec.size() * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hbest.data(), best.p, hbest.size() * 8, cudaMemcpyDeviceToHost);
+        break;
+    } while (true);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(stream);
+    if (rc != LABS_OK) return rc;
+    // emissions in g order
+    std::vector<std::pair<uint64_t, int32_t>> hits(hcnt);
+    for (size_t i = 0; i < hcnt; ++i)
+        hits[i] = {static_cast<uint64_t>(hrec[4 * i]) | (static_cast<uint64_t>(hrec[4 * i + 1]) << 32),
+                   static_cast<int32_t>(hrec[4 * i + 2])};
+    std::sort(hits.begin(), hits.end());
+    for (const auto& h : hits)
+        if (emit && emit(user, h.first, h.second) != 0) {
+            set_error("enumeration callback aborted");
+            return LABS_EABORT;
+        }
+    int64_t be = hbest[0];
+    uint64_t bg = static_cast<uint64_t>(hbest[1]);
+    for (uint64_t c = 1; c < P.nchunks; ++c)
+        if (hbest[2 * c] < be) {  // chunks in g order: strict < keeps the first g
+            be = hbest[2 * c];
+            bg = static_cast<uint64_t>(hbest[2 * c + 1]);
+        }
+    st.best_energy = be;
+    st.best_g = bg;
+    st.configurations = g_end - g_begin;
+    st.emitted = hcnt;
+    st.kernel_ms = ms_total;
+    if (stats) *stats = st;
+    return LABS_OK;
+}
+
+}  // namespace labs_b200
+
+extern "C" int labs_enumerate_class(int32_t length, int32_t prefix_len, int32_t class_index,
+                                    int32_t m, int64_t energy_threshold, uint64_t g_begin,
+                                    uint64_t g_end, labs_enum_fn emit, void* user,
+                                    labs_enum_stats* stats) {
+    return labs_b200::enumerate_class_gpu(length, prefix_len, class_index, m, energy_threshold,
+                                          g_begin, g_end, emit, user, stats, 0);
 }

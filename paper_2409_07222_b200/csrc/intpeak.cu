@@ -5,7 +5,7 @@
 //   imad  : IMAD  (fma pipe)                 d = a*d + b
 //   ialu  : LOP3/IADD3 (alu pipe)            d = (d ^ a) + b  -> IADD3/LOP3 mix
 //   mixed : 1 IMAD + 1 LOP3 per step (both pipes)
-//   dp4a  : IDP4A                            d = dp4a(a, d, d)
+//   dp4a  : IDP4A only                       d = dp4a(a, b, d)  (4 int8 MACs per lane)
 // Each counts 1 "INT32 op" per lane per instruction (an IMAD is one op here, as
 // in BASELINE.md §2's 8-ops-per-lag-term count).
 #include <cuda_runtime.h>
@@ -78,7 +78,7 @@ __global__ void k_dp4a(int* out, int a, int b) {
     for (int c = 0; c < kChains; ++c) d[c] = threadIdx.x + c;
     for (int i = 0; i < kIters; ++i) {
 #pragma unroll
-        for (int c = 0; c < kChains; ++c) d[c] = __dp4a(a, d[c] ^ b, d[c]);
+        for (int c = 0; c < kChains; ++c) d[c] = __dp4a(a, b, d[c]);
     }
     int s = 0;
 #pragma unroll
@@ -129,7 +129,7 @@ extern "C" int labs_int32_peak(double* imad_ops, double* ialu_ops, double* mixed
     const double r_imad = time_kernel(k_imad, blocks, threads, dout, per);
     const double r_ialu = time_kernel(k_ialu, blocks, threads, dout, per * 3);
     const double r_mixed = time_kernel(k_mixed, blocks, threads, dout, per * 4);
-    const double r_dp4a = time_kernel(k_dp4a, blocks, threads, dout, per * 2);
+    const double r_dp4a = time_kernel(k_dp4a, blocks, threads, dout, per);  // IDP4A lane-instr/s
     cudaFree(dout);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
