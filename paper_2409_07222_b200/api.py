@@ -19,7 +19,8 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_lib", "libpaper_labs.so")
+# LABS_B200_LIB: development override (kernel-variant A/B timing); default is the in-tree build
+_LIB_PATH = os.environ.get("LABS_B200_LIB") or os.path.join(_HERE, "_lib", "libpaper_labs.so")
 
 LABS_OK, LABS_EINVAL, LABS_ERANGE, LABS_ENODEV, LABS_ECUDA, LABS_ELOGIC, LABS_EABORT = (
     0, -1, -2, -3, -4, -5, -6)

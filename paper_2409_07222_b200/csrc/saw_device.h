@@ -16,6 +16,7 @@ constexpr int kRecHeader = 4;      // record header words: walk, iteration, ener
 //            (KH only maintained while some |C| > 127)
 //   C16    : int16 C_{2t}, t = 1..4S (pairs per word)
 //   KQ     : int32 per half index a: 16 N(a) + 32 Q(a)  (a < k),  4 N + 8 Q (a = k)
+//   DC     : word 0 = 0, then the last step's dc per lag (byte t-1 of words 1.. = lag t)
 //   HALF   : packed current half,  BLOOM : visited filter bits
 struct WalkParams {
     int32_t L, k, kp1, p;          // L = 2k+1, half length k+1, prefix length p
@@ -32,7 +33,7 @@ struct WalkParams {
     int64_t t_i;                   // iteration cap
     int64_t e_l;                   // sieve: emit iff E < e_l
     int32_t warp_words;            // shared-memory words per walk (warp)
-    int32_t off_x1, off_kl, off_kh, off_c16, off_kq, off_half, off_bloom;  // X0 at 0
+    int32_t off_x1, off_kl, off_kh, off_c16, off_kq, off_dc, off_half, off_bloom;  // X0 at 0
     int32_t warps_per_block;
     int32_t debug_check;           // re-derive E from C every iteration, flag divergence
     int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)

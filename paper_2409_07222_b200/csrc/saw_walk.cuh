@@ -1,0 +1,674 @@
+// saw_walk.cuh -- K1, the sm_100a walk kernel of Step 1 of the dual-step LABS search
+// (templates; instantiated per R in saw_walk_r*.cu, launched from saw_kernels.cu).
+//
+// K1 saw_walk_kernel : one warp = one self-avoiding walk (run_walk, saw.cpp:117-149).
+//                      Fuses the Bloom probe, the skew flip-delta of every free
+//                      neighbour (skew_flip_delta_fast, skew.cpp:60-93), the
+//                      lexicographic argmin (best_neighbour, saw.cpp:106-115), the
+//                      apply (apply_skew_flip, skew.cpp:95-105), the Bloom insert
+//                      and the E < E_l sieve with compaction into a device
+//                      record buffer (sink.emit, saw.cpp:143-146).
+// K3 saw_seed_kernel : xoshiro256** streams -> initial halves
+//                      (Rng + init_partitioned_sequence, rng.hpp:21-45, saw.cpp:65-75).
+//
+// Arithmetic.  For a skew-symmetric pivot the four sign products of
+// the reference's fused delta pair up (x_b x_{b+-kk} = x_a x_{a-+kk}), so for half
+// index a < k (b = L-1-a):
+//     dE(a) = 16 N(a) + 32 Q(a) - 8 x_a G(a) + 8 (-1)^(k-a) C_{2(k-a)}
+// and for the centre a = k:  dE = 4 N + 8 Q - 4 x_k G, where
+//     G(a) = sum_{j = a mod 2, j != a} C_{|a-j|} x_j      (x = 0 outside [0, L))
+//     N(a) = #valid single terms,  Q(a) = sum_t x_{a-2t} x_{a+2t} (b excluded).
+// G is the only O(L) part.  On the parity array X_par it is a sliding dot product with
+// the symmetric kernel K[d] = C_{2|d|}: G(a) = sum_i X_par[i] K[i - a/2].  A lane owns
+// neighbours a0, a0+8, ..., so one X word is shared by its R neighbours and the kernel
+// window slides by one word per neighbour: 4 positions per IDP4A (int8 C), plus a
+// second IDP4A on the high bytes while some |C| > 127.  16N+32Q is kept per neighbour
+// in shared memory and updated in O(1) per flip.  Everything is exact integer math.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "saw_device.h"
+#include "saw_walk.h"
+
+namespace labs_b200 {
+
+#define FULLMASK 0xffffffffu
+#define INT_BIG 0x7fffffff
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    return __byte_perm(a, b, sel);
+}
+
+// (h1 + i*h2) mod 2^64 mod m  (bloom.cpp:28,36), Barrett with mu = floor(2^64/m), m < 2^32
+__device__ __forceinline__ uint32_t bloom_index(uint64_t h1, uint64_t h2, uint32_t i, uint64_t mu,
+                                                uint32_t m) {
+    const uint64_t x = h1 + (uint64_t)i * h2;
+    const uint64_t q = __umul64hi(x, mu);
+    const uint64_t r = x - q * (uint64_t)m;
+    return (uint32_t)(r >= m ? r - m : r);
+}
+
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int lane_mask) {
+    const uint32_t lo = __shfl_xor_sync(FULLMASK, (uint32_t)v, lane_mask);
+    const uint32_t hi = __shfl_xor_sync(FULLMASK, (uint32_t)(v >> 32), lane_mask);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_sum64(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += (long long)shfl_xor64((uint64_t)v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t sel4(int o) {  // bytes o..o+3 of a word pair
+    return (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+}
+__device__ __forceinline__ uint32_t sel4r(int o) {  // bytes o+3..o (reversed)
+    return (uint32_t)((o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
+}
+// sign-extended byte b of w
+__device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
+
+// ---------------------------------------------------------------------------
+// Main O(L) loop: G(a) for this lane's R neighbours a = a0 + 8m (a' = a0' + 4m).
+// Step w: X word w (positions 4w..4w+3 of the lane's parity) is shared by all R
+// neighbours; neighbour m needs kernel bytes koff + 4(w-m) - a0' .. +3, i.e. the
+// PRMT-aligned word KW_{w-m}; KW slides one slot per step (one new raw word).
+template <int R, bool WIDE>
+__device__ __forceinline__ void g_step(const uint32_t* __restrict__ Xw,
+                                       const uint32_t* __restrict__ Kl,
+                                       const uint32_t* __restrict__ Kh, int w, int j, int kb,
+                                       uint32_t sel, uint32_t (&KL)[R], uint32_t (&KH)[R],
+                                       uint32_t& rl, uint32_t& rh, int (&acc)[R],
+                                       int (&acch)[R]) {
+    const uint32_t x = Xw[w];
+    const uint32_t nl = Kl[kb + w + 2];
+    uint32_t nh = 0;
+    if (WIDE) nh = Kh[kb + w + 2];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        acc[m] = __dp4a((int)x, (int)KL[(j - m + R) % R], acc[m]);
+        if (WIDE) acch[m] = __dp4a((int)x, (int)KH[(j - m + R) % R], acch[m]);
+    }
+    KL[(j + 1) % R] = prmt(rl, nl, sel);
+    rl = nl;
+    if (WIDE) {
+        KH[(j + 1) % R] = prmt(rh, nh, sel);
+        rh = nh;
+    }
+}
+
+template <int R, bool WIDE>
+__device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
+                                             const uint32_t* __restrict__ Kl,
+                                             const uint32_t* __restrict__ Kh, int nwx, int kb,
+                                             uint32_t sel, int (&acc)[R], int (&acch)[R]) {
+    uint32_t KL[R], KH[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        KL[(R - m) % R] = prmt(Kl[kb - m], Kl[kb - m + 1], sel);
+        if (WIDE) KH[(R - m) % R] = prmt(Kh[kb - m], Kh[kb - m + 1], sel);
+        acc[m] = 0;
+        acch[m] = 0;
+    }
+    uint32_t rl = Kl[kb + 1], rh = 0;
+    if (WIDE) rh = Kh[kb + 1];
+    const int nfull = (nwx / R) * R;
+    for (int w0 = 0; w0 < nfull; w0 += R) {
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+            g_step<R, WIDE>(Xw, Kl, Kh, w0 + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
+    }
+    if (nfull < nwx) {
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+            if (nfull + j < nwx)
+                g_step<R, WIDE>(Xw, Kl, Kh, nfull + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
+    }
+}
+
+// ---------------------------------------------------------------------------
+struct WarpSmem {
+    int8_t* X0;       // parity arrays (byte views, index xoff + i)
+    int8_t* X1;
+    uint32_t* X0w;
+    uint32_t* X1w;
+    uint32_t* KL;     // kernel low bytes (word view)
+    uint32_t* KH;     // kernel high bytes
+    uint32_t* C16;    // int16 C_{2t}, t = 4s+1..4s+4 in words 2s, 2s+1
+    int* KQ;          // 16N+32Q per half index (walk initialisation only)
+    uint32_t* DC;     // dc of the last step per lag, byte t-1 = lag t; DC[-1] = 0
+    uint32_t* half;   // half bits
+    uint32_t* bloom;  // visited filter
+};
+
+__device__ __forceinline__ int xval(const WarpSmem& w, const WalkParams& P, int j) {
+    return (j & 1) ? w.X1[P.xoff + (j >> 1)] : w.X0[P.xoff + (j >> 1)];
+}
+
+// Sign of full-sequence position j of the skew expansion of `half` (skew.cpp:14-26).
+__device__ __forceinline__ int x_of_half(const uint32_t* half, int k, int j) {
+    int src = j, neg = 0;
+    if (j > k) {
+        const int i = j - k;
+        src = k - i;
+        neg = i & 1;
+    }
+    const int bit = (half[src >> 5] >> (src & 31)) & 1;
+    return (bit ^ neg) ? 1 : -1;
+}
+
+// C_{2t} by direct summation over the parity arrays (sequence.cpp:8-19 restricted to
+// even lags; odd lags of a skew sequence vanish): sum_par sum_i X[i] X[i+t].
+__device__ __forceinline__ int corr_even_lag(const WarpSmem& w, const WalkParams& P, int t) {
+    int acc = 0;
+    const int dw = t >> 2;
+    const uint32_t sel = sel4(t & 3);
+    const int n0 = P.xoff >> 2;
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+        const uint32_t* Xw = par ? w.X1w : w.X0w;
+        for (int n = n0; n < n0 + P.nwx; ++n)
+            acc = __dp4a((int)Xw[n], (int)prmt(Xw[n + dw], Xw[n + dw + 1], sel), acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ uint32_t pack4(int b0, int b1, int b2, int b3) {  // low bytes
+    return prmt(prmt((uint32_t)b0, (uint32_t)b1, 0x0040), prmt((uint32_t)b2, (uint32_t)b3, 0x0040),
+                0x5410);
+}
+__device__ __forceinline__ int hi_byte(int c) { return (c - (int)(int8_t)c) >> 8; }
+
+// Store the 4 correlations c[0..3] of lag word s (t = 4s+1..4s+4) into C16 and the
+// kernel arrays: forward word (d = 4s+1..4s+4) = (c0,c1,c2,c3); mirrored word
+// (d = -4s-3..-4s) = (c2,c1,c0,cprev) with cprev = C_{2*4s} (0 for s = 0: K[0] = 0).
+__device__ __forceinline__ void store_c_word(const WarpSmem& w, const WalkParams& P, int s,
+                                             const int (&c)[4], int cprev, bool wide) {
+    w.C16[2 * s] = prmt((uint32_t)c[0], (uint32_t)c[1], 0x5410);
+    w.C16[2 * s + 1] = prmt((uint32_t)c[2], (uint32_t)c[3], 0x5410);
+    const int fw = (P.koff + 1) / 4 + s;
+    const int bw = (P.koff - 3) / 4 - s;
+    w.KL[fw] = pack4(c[0], c[1], c[2], c[3]);
+    w.KL[bw] = pack4(c[2], c[1], c[0], cprev);
+    if (wide) {
+        w.KH[fw] = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[bw] = pack4(hi_byte(c[2]), hi_byte(c[1]), hi_byte(c[0]), hi_byte(cprev));
+    }
+}
+
+// Kernel words of lag word s without the int16 copy (main loop: C lives in registers).
+__device__ __forceinline__ void store_k_word(const WarpSmem& w, const WalkParams& P, int s,
+                                             const int (&c)[4], int cprev, bool wide) {
+    const int fw = (P.koff + 1) / 4 + s;
+    const int bw = (P.koff - 3) / 4 - s;
+    w.KL[fw] = pack4(c[0], c[1], c[2], c[3]);
+    w.KL[bw] = pack4(c[2], c[1], c[0], cprev);
+    if (wide) {
+        w.KH[fw] = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[bw] = pack4(hi_byte(c[2]), hi_byte(c[1]), hi_byte(c[0]), hi_byte(cprev));
+    }
+}
+
+template <int R>
+struct LagWords {  // lag words a lane may own: s = lane + 32 jj, S <= 4*ceil((32R+29)/128)*32
+    static constexpr int value = (32 * R + 29 + 127) / 128 < 4 ? (32 * R + 29 + 127) / 128 : 4;
+};
+
+// K1: one warp = one walk.  v3 bookkeeping: the per-neighbour constant part of the delta
+//     T(a) = 16 N(a) + 32 Q(a) + 8 (-1)^(k-a) C_{2(k-a)}   (a < k),   4 N + 8 Q  (a = k)
+// and xs(a) = 8 x_a (4 x_k) live in the owning lane's registers, so a delta is one IMAD on
+// the sliding dot product G(a): dE(a) = T(a) - xs(a) G(a).  Per step T is updated in O(1)
+// per neighbour (Q pairs through the flipped positions, and the C term from the per-lag
+// dc bytes the C update publishes); the exact even-lag C live in the lag owners' registers.
+template <int R, bool COUNT>
+__device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint64_t* fm0,
+                              const uint64_t* fm1, int64_t walk, int lane, int* score_out,
+                              int* corr_out) {
+    constexpr int NJ = LagWords<R>::value;
+    const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
+    const int nj = (S + 31) >> 5;  // lag words owned per lane (<= NJ)
+
+    // ---- load the initial half, build parity arrays, clear kernel + Bloom ----
+    const uint32_t* src = P.halves + walk * P.hw;
+    for (int i = lane; i < P.hw; i += 32) w.half[i] = src[i];
+    __syncwarp();
+    for (int wi = lane; wi < 2 * P.xwords; wi += 32) {
+        const int par = wi >= P.xwords;
+        const int word = wi - par * P.xwords;
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int li = word * 4 + b - P.xoff;
+            const int j = 2 * li + par;
+            const int x = (li >= 0 && j < L) ? x_of_half(w.half, k, j) : 0;
+            v |= ((uint32_t)x & 0xffu) << (8 * b);
+        }
+        (par ? w.X1w : w.X0w)[word] = v;
+    }
+    for (int i = lane; i < 2 * P.kwords; i += 32) w.KL[i] = 0;  // KL and KH are adjacent
+    if (lane == 0) w.DC[-1] = 0;  // dc of "lag 0" (the centre neighbour has no C term)
+    {
+        uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
+        for (int i = lane; i < (P.bloom_words >> 2); i += 32) b4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
+    // ---- exact C_{2t} of the owned lag words (registers), E, max|C| ----
+    int e_part = 0, cmax = 0;
+    int C[NJ][4];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) {
+        const int s = lane + 32 * jj;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int t = 4 * s + 1 + b;
+            int v = 0;
+            if (jj < nj && s < S && t <= k) v = corr_even_lag(w, P, t);
+            C[jj][b] = v;
+            e_part += v * v;
+            cmax = max(cmax, abs(v));
+        }
+    }
+    int energy = warp_sum(e_part);
+    bool wide = __reduce_max_sync(FULLMASK, (unsigned)cmax) > 127u;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) {
+        const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1);
+        const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, 31);
+        const int s = lane + 32 * jj;
+        const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
+        if (jj < nj && s < S) {
+            store_c_word(w, P, s, C[jj], cprev, wide);
+            if (corr_out)
+                for (int b = 0; b < 4; ++b)
+                    if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = C[jj][b];
+        }
+    }
+
+    // ---- 16N + 32Q per half index (lanes over a), once per walk ----
+    for (int a = P.p + lane; a <= k; a += 32) {
+        const int8_t* Xb = ((a & 1) ? w.X1 : w.X0) + P.xoff + (a >> 1);
+        const int tstar = (a < k) ? (k - a) : -1;
+        int q = 0;
+        for (int t = 1; 2 * t <= a; ++t)
+            if (t != tstar) q += (int)Xb[-t] * (int)Xb[t];
+        const int n = (a >> 1) + ((L - 1 - a) >> 1) - (a < k ? 1 : 0);
+        w.KQ[a] = (a < k) ? 16 * n + 32 * q : 4 * n + 8 * q;
+    }
+    __syncwarp();
+
+    // ---- lane geometry: this lane's neighbours a = a0 + 8m (all of parity `par`) ----
+    const int cgrp = lane & 7, g = lane >> 3;
+    const int a0 = P.p + cgrp + 8 * R * g;
+    const int par = a0 & 1, a0h = a0 >> 1;
+    const uint32_t* Xw = (par ? w.X1w : w.X0w) + (P.xoff >> 2);
+    const int8_t* Xmine = (par ? w.X1 : w.X0) + P.xoff;
+    const int kb = (P.koff - a0h) >> 2;
+    const uint32_t ksel = sel4((P.koff - a0h) & 3);
+    const int sgn8 = ((k - a0) & 1) ? -8 : 8;  // 8 (-1)^(k-a), the same for every m
+    const uint32_t kbase = 0x80000000u + (uint32_t)a0;  // key = (dE + 2^22) * 512 + a
+    int T[R], xs[R];  // (meaningless for a > k: those are masked by `inval`)
+    {
+        const int16_t* C16h = reinterpret_cast<const int16_t*>(w.C16);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int a = a0 + 8 * m;
+            T[m] = 0;
+            xs[m] = 0;
+            if (a < k) {
+                T[m] = w.KQ[a] + sgn8 * (int)C16h[k - a - 1];
+                xs[m] = 8 * (int)Xmine[a >> 1];
+            } else if (a == k) {
+                T[m] = w.KQ[a];
+                xs[m] = 4 * (int)Xmine[a >> 1];
+            }
+        }
+    }
+    const int8_t* DCb = reinterpret_cast<const int8_t*>(w.DC);  // byte t-1 = dc of lag t
+
+    // ---- half hashes h1, h2 (saw.cpp:77-89) and the initial Bloom insert ----
+    uint64_t h1 = 0, h2 = 0;
+    for (int i = lane; i < kp1; i += 32) {
+        const int bit = (w.half[i >> 5] >> (i & 31)) & 1;
+        h1 ^= P.tab[(0 * kp1 + i) * 2 + bit];
+        h2 ^= P.tab[(1 * kp1 + i) * 2 + bit];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h1 ^= shfl_xor64(h1, o);
+        h2 ^= shfl_xor64(h2, o);
+    }
+    h1 ^= P.salt0;
+    h2 ^= P.salt1;
+    if (lane < P.bloom_k) {
+        const uint32_t idx = bloom_index(h1, h2, lane, P.bloom_mu, P.bloom_bits);
+        atomicOr(&w.bloom[idx >> 5], 1u << (idx & 31));
+    }
+    __syncwarp();
+
+    const int e0 = energy;
+    int best = energy;
+    long long iterations = 0, emitted = 0, probes = 0, wide_iters = 0, diverged = 0;
+    long long evals_part = 0;  // per-lane unvisited-neighbour count (COUNT mode)
+    int exhausted = 0;
+    // lane-local neighbours excluded from the argmin: a > k (not neighbours) and the undo
+    // move of the last step (the previous pivot is always in the filter)
+    uint32_t inval = 0;
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+        if (a0 + 8 * m > k) inval |= 1u << m;
+    uint32_t skip = inval;
+    const int64_t t_i = score_out ? 1 : P.t_i;
+
+    for (long long it = 0; it < t_i; ++it) {
+        // ---- G for all owned neighbours (the O(L) part: IDP4A sliding dot product) ----
+        int acc[R], acch[R];
+        if (wide) {
+            g_neighbours<R, true>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
+            ++wide_iters;
+        } else {
+            g_neighbours<R, false>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
+        }
+        // ---- exact deltas: dE(a) = T(a) - xs(a) G(a) ----
+        int delta[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int gg = wide ? acc[m] + 256 * acch[m] : acc[m];
+            delta[m] = T[m] - xs[m] * gg;
+        }
+        if (score_out) {
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                if (a0 + 8 * m <= k) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
+            break;
+        }
+
+        // ---- choose: lowest (delta, hp) among unvisited (best_neighbour, saw.cpp:106-115) ----
+        if (COUNT) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (a0 + 8 * m > k) continue;  // in `inval`
+                const int a = a0 + 8 * m;
+                const uint64_t n1 = h1 ^ fm0[a], n2 = h2 ^ fm1[a];
+                bool hit = true;
+                for (int i = 0; i < P.bloom_k; ++i) {
+                    const uint32_t idx = bloom_index(n1, n2, i, P.bloom_mu, P.bloom_bits);
+                    if (!((w.bloom[idx >> 5] >> (idx & 31)) & 1)) {
+                        hit = false;
+                        break;
+                    }
+                }
+                if (hit) skip |= 1u << m;
+                else ++evals_part;
+            }
+        }
+        // lane minimum, lowest m first; `skip` excludes the undo move (the previous pivot
+        // is always in the filter) without a Bloom probe, and the non-neighbours a > k.
+        // For L <= 1001, |dE| < 2^22 and one unsigned key (dE + 2^22) << 9 | a orders
+        // (delta, hp) lexicographically, so one REDUX finds the winner.
+        int dstar = 0, astar = -1;
+        uint32_t ins_idx = 0;  // Bloom bit of the accepted neighbour, reused for the insert
+        const bool one_key = L <= 1001;
+        uint32_t bkey = 0xffffffffu;
+        int bd = INT_BIG, bm = 0;
+        if (one_key) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const uint32_t key = (skip & (1u << m)) ? 0xffffffffu
+                                                        : (uint32_t)delta[m] * 512u + kbase + 8u * m;
+                bkey = min(bkey, key);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                if (!(skip & (1u << m)) && delta[m] < bd) {
+                    bd = delta[m];
+                    bm = m;
+                }
+        }
+        while (true) {
+            int md, ma;
+            bool mine_won;
+            if (one_key) {
+                const uint32_t k_best = __reduce_min_sync(FULLMASK, bkey);
+                if (k_best == 0xffffffffu) break;  // every free neighbour visited
+                ma = (int)(k_best & 511u);
+                md = (int)(k_best >> 9) - (1 << 22);
+                mine_won = bkey == k_best;
+            } else {
+                md = __reduce_min_sync(FULLMASK, bd);
+                if (md == INT_BIG) break;
+                const int mine = (bd == md) ? a0 + 8 * bm : INT_BIG;
+                ma = __reduce_min_sync(FULLMASK, mine);
+                mine_won = mine == ma;
+            }
+            const uint64_t n1 = h1 ^ fm0[ma], n2 = h2 ^ fm1[ma];
+            bool bit = true;
+            if (lane < P.bloom_k) {
+                ins_idx = bloom_index(n1, n2, lane, P.bloom_mu, P.bloom_bits);
+                bit = (w.bloom[ins_idx >> 5] >> (ins_idx & 31)) & 1;
+            }
+            if (COUNT) {  // already filtered: the minimum is unvisited
+                dstar = md;
+                astar = ma;
+                break;
+            }
+            ++probes;
+            if (__all_sync(FULLMASK, bit)) {
+                if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
+                    skip |= 1u << ((ma - a0) >> 3);
+                    bkey = 0xffffffffu;
+                    bd = INT_BIG;
+                    bm = 0;
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        if (skip & (1u << m)) continue;
+                        bkey = min(bkey, (uint32_t)delta[m] * 512u + kbase + 8u * m);
+                        if (delta[m] < bd) {
+                            bd = delta[m];
+                            bm = m;
+                        }
+                    }
+                }
+                continue;
+            }
+            dstar = md;
+            astar = ma;
+            break;
+        }
+        if (astar < 0) {
+            exhausted = 1;
+            break;
+        }
+
+        // ---- apply the skew flip at astar (apply_skew_flip, skew.cpp:95-105) ----
+        ++iterations;
+        const bool cen = astar == k;
+        const int bstar = L - 1 - astar;
+        const int apar = astar & 1, ah = astar >> 1;
+        int8_t* Xa = (apar ? w.X1 : w.X0) + P.xoff;
+        const int xa = Xa[ah];
+        const int xb = cen ? 0 : (((k - astar) & 1) ? -xa : xa);
+        const int dstar_l = astar - a0;  // == 8m for the owner of astar
+        // (1) zero x_a and x_b: the Q pairs below and the C windows then read 0 there,
+        //     which is exactly the fused rule's treatment of the flipped pair
+        __syncwarp();
+        if (lane == 0) Xa[ah] = 0;
+        if (lane == 1) Xa[bstar >> 1] = 0;
+        __syncwarp();
+        // (2) Q pairs through the flipped positions, neighbours of astar's parity:
+        //     dQ(a) = -x_a* x_{2a-a*} - x_b* x_{2a-b*}, except the pair excluded from Q(a)
+        //     (its upper element is L-1-a, i.e. a* = 3a - (L-1)).  The centre's Q never
+        //     changes (its only pair through a* is (a*, b*), both zeroed).
+        skip = inval;
+        if (par == apar) {  // (the owner of astar has astar's parity)
+            const int ex3 = astar + L - 1;  // == 3a for the excluded pair
+            const int8_t* Xp = Xa + ((2 * a0 - astar) >> 1);
+            const int8_t* Xq = Xa + ((2 * a0 - bstar) >> 1);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                int xp = Xp[8 * m];
+                const int xq = Xq[8 * m];
+                if (3 * (a0 + 8 * m) == ex3) xp = 0;
+                const int term = xa * xp + xb * xq;
+                if (dstar_l != 8 * m) {
+                    T[m] -= 64 * term;
+                } else {  // the pivot's own entry: its sign flips; next step's undo move
+                    xs[m] = -xs[m];
+                    skip |= 1u << m;
+                }
+            }
+        }
+        // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
+        int cmx = 0, esp = 0;
+        {
+            const uint32_t* Xaw = apar ? w.X1w : w.X0w;
+            const int awF = (P.xoff + ah + 1) >> 2;
+            const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
+            const int awB = (P.xoff + ah - 4) >> 2;
+            const uint32_t asB = sel4r((P.xoff + ah) & 3);
+            const int mul = cen ? -2 * xa : -4 * xa;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int s = lane + 32 * jj;
+                if (jj < nj && s < S) {
+                    const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
+                    const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
+                    int dc[4];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        dc[b] = mul * (sbyte(fw, b) + sbyte(bw, b));
+                        C[jj][b] += dc[b];
+                        cmx |= C[jj][b] + 128;  // bits above 7 set <=> |C| > 127 somewhere
+                        if (P.debug_check) esp += C[jj][b] * C[jj][b];
+                    }
+                    w.DC[s] = pack4(dc[0], dc[1], dc[2], dc[3]);
+                }
+            }
+        }
+        const bool wide_next = __any_sync(FULLMASK, (cmx & ~0xff) != 0);  // also syncs
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1);
+            const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, 31);
+            const int s = lane + 32 * jj;
+            const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
+            if (jj < nj && s < S) store_k_word(w, P, s, C[jj], cprev, wide_next);
+        }
+        wide = wide_next;
+        __syncwarp();
+        // (4) write the flipped pair, C term of T, sign of the pivot's own entry, hashes
+        if (lane == 0) Xa[ah] = (int8_t)(-xa);
+        if (lane == 1 && !cen) Xa[bstar >> 1] = (int8_t)(-xb);
+        if (lane == 2) w.half[astar >> 5] ^= 1u << (astar & 31);
+        {
+            const int8_t* Dm = DCb + (k - a0 - 1);  // byte t-1 of lag t = k - a
+#pragma unroll
+            for (int m = 0; m < R; ++m) T[m] += sgn8 * (int)Dm[-8 * m];
+        }
+        if (P.debug_check) {
+            const int echk = warp_sum(esp);
+            if (echk != energy + dstar) ++diverged;
+        }
+        h1 ^= fm0[astar];
+        h2 ^= fm1[astar];
+        if (lane < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
+        energy += dstar;
+        best = min(best, energy);
+        __syncwarp();
+        if (energy < P.e_l) {
+            ++emitted;
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(P.rec_count, 1ull);
+            slot = __shfl_sync(FULLMASK, slot, 0);
+            if ((long long)slot < P.rec_cap) {
+                uint32_t* r = P.rec + slot * (unsigned long long)P.rec_words;
+                if (lane == 0) {
+                    r[0] = (uint32_t)walk;
+                    r[1] = (uint32_t)(it + 1);
+                    r[2] = (uint32_t)energy;
+                    r[3] = 0;
+                }
+                for (int i = lane; i < P.hw; i += 32) r[kRecHeader + i] = w.half[i];
+            }
+        }
+    }
+    if (COUNT) evals_part = warp_sum64(evals_part);
+    if (lane == 0 && P.walk_stats) {
+        int64_t* st = P.walk_stats + walk * kWalkStatWords;
+        st[kWsIterations] = iterations;
+        st[kWsEmitted] = emitted;
+        st[kWsBest] = best;
+        st[kWsInitial] = e0;
+        st[kWsExhausted] = exhausted;
+        st[kWsDeltaEvals] = COUNT ? evals_part : -1;
+        st[kWsVisitedProbes] = probes;
+        st[kWsWideIters] = wide_iters;
+        st[kWsDiverged] = diverged;
+    }
+    __syncwarp();
+}
+
+#ifndef LABS_MIN_BLOCKS
+#define LABS_MIN_BLOCKS 4
+#endif
+template <int R, bool COUNT>
+__global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkParams P, int* score_out,
+                                                                        int* corr_out) {
+    extern __shared__ uint4 smem_u4[];
+    uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
+    for (int i = threadIdx.x; i < 2 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
+    __syncthreads();
+    const int fm_words = ((2 * P.kp1 * 2) + 3) & ~3;  // u32 words, 16-byte aligned
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + fm_words + warp * P.warp_words;
+    WarpSmem w;
+    w.X0w = base;
+    w.X1w = base + P.off_x1;
+    w.X0 = reinterpret_cast<int8_t*>(w.X0w);
+    w.X1 = reinterpret_cast<int8_t*>(w.X1w);
+    w.KL = base + P.off_kl;
+    w.KH = base + P.off_kh;
+    w.C16 = base + P.off_c16;
+    w.KQ = reinterpret_cast<int*>(base + P.off_kq);
+    w.DC = base + P.off_dc + 1;
+    w.half = base + P.off_half;
+    w.bloom = base + P.off_bloom;
+    const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
+    for (int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp; walk < P.nwalks;
+         walk += stride)
+        run_walk_warp<R, COUNT>(P, w, fm, fm + P.kp1, walk, lane, score_out, corr_out);
+}
+
+// Per-R launch / occupancy helpers, explicitly instantiated in saw_walk_r*.cu so that
+// the sixteen R variants compile in parallel translation units.
+template <int R>
+cudaError_t launch_walk_fixed(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
+                              int* score_out, int* corr_out, bool count) {
+    auto kfn = count ? saw_walk_kernel<R, true> : saw_walk_kernel<R, false>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, P.warps_per_block * 32, smem, st>>>(P, score_out, corr_out);
+    return cudaGetLastError();
+}
+
+template <int R>
+int blocks_per_sm_fixed(const WalkParams& P, size_t smem) {
+    int n = 0;
+    cudaFuncSetAttribute(saw_walk_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, saw_walk_kernel<R, false>,
+                                                      P.warps_per_block * 32, smem) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+}  // namespace labs_b200
