@@ -76,6 +76,24 @@ typedef struct labs_candidate {
 /* CandidateSink::emit (candidate.hpp:56-60). Return 0 to continue, nonzero to abort. */
 typedef int (*labs_candidate_fn)(void* user, const labs_candidate* c);
 
+/* A batch of candidates (same order and semantics as labs_candidate_fn deliveries).
+ * Arrays valid only during the callback; signs is count x length, row i the full
+ * expanded sequence; prefix_class[i] indexes prefixes (P x prefix_len, rank order). */
+typedef struct labs_candidate_batch {
+    int32_t count;
+    int32_t length;
+    int32_t prefix_len;
+    int32_t origin;            /* 0 = saw */
+    const int8_t* signs;
+    const int64_t* energy;
+    const int64_t* walker;
+    const int64_t* restart;
+    const int64_t* iteration;
+    const int32_t* prefix_class;
+    const int8_t* prefixes;
+} labs_candidate_batch;
+typedef int (*labs_candidate_batch_fn)(void* user, const labs_candidate_batch* batch);
+
 /* PoolStats (saw.hpp:161-167) + GPU counters */
 typedef struct labs_pool_stats {
     int64_t walks;
@@ -103,6 +121,10 @@ typedef struct labs_pool_stats {
  * to the reference's --threads 1 run. */
 int labs_saw_pool_run(const labs_saw_config* cfg, labs_candidate_fn emit, void* user,
                       labs_pool_stats* stats);
+/* Same, delivering candidates in batches (<= 8192 per call) -- cheaper across FFI
+ * boundaries (the Python binding uses it). */
+int labs_saw_pool_run_batched(const labs_saw_config* cfg, labs_candidate_batch_fn emit, void* user,
+                              labs_pool_stats* stats);
 
 /* Derived configuration (saw.cpp:44-63, sequence.cpp:36-40, bloom.cpp:15-24). */
 typedef struct labs_saw_derived {

@@ -97,7 +97,18 @@ class _EnumStats(C.Structure):
     ]
 
 
+class _CandidateBatch(C.Structure):
+    _fields_ = [
+        ("count", C.c_int32), ("length", C.c_int32), ("prefix_len", C.c_int32),
+        ("origin", C.c_int32), ("signs", C.POINTER(C.c_int8)), ("energy", C.POINTER(C.c_int64)),
+        ("walker", C.POINTER(C.c_int64)), ("restart", C.POINTER(C.c_int64)),
+        ("iteration", C.POINTER(C.c_int64)), ("prefix_class", C.POINTER(C.c_int32)),
+        ("prefixes", C.POINTER(C.c_int8)),
+    ]
+
+
 _CAND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_Candidate))
+_BATCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_CandidateBatch))
 _REC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int8),
                       C.c_int32)
 _ENUM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int64)
@@ -124,6 +135,8 @@ def load_library():
         lib.labs_version.restype = C.c_char_p
         lib.labs_saw_pool_run.argtypes = [C.POINTER(_Config), _CAND_FN, C.c_void_p,
                                           C.POINTER(_PoolStats)]
+        lib.labs_saw_pool_run_batched.argtypes = [C.POINTER(_Config), _BATCH_FN, C.c_void_p,
+                                                  C.POINTER(_PoolStats)]
         lib.labs_saw_derive.argtypes = [C.POINTER(_Config), C.POINTER(_Derived)]
         lib.labs_saw_walks.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double,
                                        C.POINTER(C.c_int8), C.c_int64, C.c_int32, C.c_int32,
@@ -253,21 +266,48 @@ class CandidateSink:
 
 
 class CollectingSink(CandidateSink):
+    """candidate.hpp:62-80.  Batches from the engine are kept as arrays and turned into
+    Candidate objects only when taken."""
+
     def __init__(self):
         self.items: List[Candidate] = []
+        self._batches: list = []
         self._mu = threading.Lock()
 
     def emit(self, c: Candidate) -> None:
         with self._mu:
+            self._materialise()
             self.items.append(c)
+
+    def emit_batch(self, signs, energy, walker, restart, iteration, prefixes) -> None:
+        with self._mu:
+            self._batches.append((signs, energy, walker, restart, iteration, prefixes))
+
+    def _materialise(self):
+        for signs, energy, walker, restart, iteration, prefixes in self._batches:
+            e, w, r, it = energy.tolist(), walker.tolist(), restart.tolist(), iteration.tolist()
+            self.items.extend(Candidate(signs[i], e[i], "saw", prefixes[i], w[i], r[i], it[i])
+                              for i in range(len(e)))
+        self._batches = []
+
+    def arrays(self):
+        """All collected candidates as (signs [n, L], energy [n]) without building objects."""
+        with self._mu:
+            self._materialise()
+            if not self.items:
+                return np.zeros((0, 0), dtype=np.int8), np.zeros(0, dtype=np.int64)
+            return (np.stack([c.seq for c in self.items]),
+                    np.array([c.energy for c in self.items], dtype=np.int64))
 
     def take(self) -> List[Candidate]:
         with self._mu:
+            self._materialise()
             out, self.items = self.items, []
         return out
 
     def size(self) -> int:
-        return len(self.items)
+        with self._mu:
+            return len(self.items) + sum(len(b[1]) for b in self._batches)
 
 
 class DedupSink(CandidateSink):
@@ -331,27 +371,45 @@ def derive(cfg: SawConfig) -> dict:
 
 
 def run_saw_pool(cfg: SawConfig, sink: Optional[CandidateSink] = None) -> PoolStats:
-    """run_saw_pool (saw.cpp:218-267) on the GPU; candidates in --threads 1 order."""
+    """run_saw_pool (saw.cpp:218-267) on the GPU; candidates in --threads 1 order.
+
+    Candidates cross the C ABI in batches (labs_saw_pool_run_batched); sinks with an
+    `emit_batch(signs, energy, walker, restart, iteration, prefixes)` method receive the
+    numpy arrays directly, others get one `emit(Candidate)` per candidate."""
     lib = load_library()
     err: list = []
 
-    def on_cand(user, cp):
+    def on_batch(user, bp):
         try:
-            c = cp.contents
-            seq = np.ctypeslib.as_array(c.signs, (c.length,)).copy()
-            pre = (np.ctypeslib.as_array(c.prefix, (c.prefix_len,)).copy()
-                   if c.prefix_len > 0 else np.zeros(0, dtype=np.int8))
-            if sink is not None:
-                sink.emit(Candidate(seq, int(c.energy), "saw", pre, int(c.walker),
-                                    int(c.restart), int(c.iteration)))
+            b = bp.contents
+            n, L, p = b.count, b.length, b.prefix_len
+            signs = np.ctypeslib.as_array(b.signs, (n, L)).copy()
+            energy = np.ctypeslib.as_array(b.energy, (n,)).copy()
+            walker = np.ctypeslib.as_array(b.walker, (n,)).copy()
+            restart = np.ctypeslib.as_array(b.restart, (n,)).copy()
+            iteration = np.ctypeslib.as_array(b.iteration, (n,)).copy()
+            cls = np.ctypeslib.as_array(b.prefix_class, (n,))
+            if p > 0:
+                table = np.ctypeslib.as_array(b.prefixes, (int(cls.max()) + 1, p))
+                prefixes = table[cls].copy()
+            else:
+                prefixes = np.zeros((n, 0), dtype=np.int8)
+            if sink is None:
+                return 0
+            if hasattr(sink, "emit_batch"):
+                sink.emit_batch(signs, energy, walker, restart, iteration, prefixes)
+            else:
+                for i in range(n):
+                    sink.emit(Candidate(signs[i], int(energy[i]), "saw", prefixes[i],
+                                        int(walker[i]), int(restart[i]), int(iteration[i])))
             return 0
         except BaseException as e:  # propagate after the C call returns
             err.append(e)
             return 1
 
     st = _PoolStats()
-    cb = _CAND_FN(on_cand)
-    rc = lib.labs_saw_pool_run(C.byref(cfg._c()), cb, None, C.byref(st))
+    cb = _BATCH_FN(on_batch)
+    rc = lib.labs_saw_pool_run_batched(C.byref(cfg._c()), cb, None, C.byref(st))
     if err:
         raise err[0]
     _check(rc)

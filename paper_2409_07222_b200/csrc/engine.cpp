@@ -76,6 +76,7 @@ struct WalkRecordView {
     int64_t walk;        // batch-local walk index
     int64_t iteration;
     int64_t energy;
+    uint64_t hash;       // canonical_hash(0) of the full sequence (computed on the device)
     const uint32_t* half;
 };
 
@@ -96,7 +97,7 @@ public:
     cudaEvent_t ev[4] = {};
     WalkParams wp{};
     int grid_cap = 0;
-    DevBuf<uint64_t> fm, tab, rng;
+    DevBuf<uint64_t> fm, tab, tabfull, rng;
     DevBuf<uint32_t> halves, rec, seg_walker, seg_prefix;
     DevBuf<int64_t> stats, seg_rest, seg_off;
     DevBuf<int32_t> seg_init;
@@ -119,22 +120,38 @@ public:
         LABS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         for (auto& e : ev) LABS_CUDA(cudaEventCreate(&e));
         const auto& tt = TabTables::get();
-        std::vector<uint64_t> hfm(2 * static_cast<size_t>(wp.kp1));
-        std::vector<uint64_t> htab(4 * static_cast<size_t>(wp.kp1));
+        const int kp1 = wp.kp1, L = wp.L;
+        std::vector<uint64_t> hfm(3 * static_cast<size_t>(kp1));
+        std::vector<uint64_t> htab(4 * static_cast<size_t>(kp1));
+        std::vector<uint64_t> hfull(2 * static_cast<size_t>(L));
         for (int t = 0; t < 2; ++t)
-            for (int i = 0; i < wp.kp1; ++i) {
-                hfm[static_cast<size_t>(t) * wp.kp1 + i] = tt.t[t][i][0] ^ tt.t[t][i][1];
-                htab[(static_cast<size_t>(t) * wp.kp1 + i) * 2 + 0] = tt.t[t][i][0];
-                htab[(static_cast<size_t>(t) * wp.kp1 + i) * 2 + 1] = tt.t[t][i][1];
+            for (int i = 0; i < kp1; ++i) {
+                hfm[static_cast<size_t>(t) * kp1 + i] = tt.t[t][i][0] ^ tt.t[t][i][1];
+                htab[(static_cast<size_t>(t) * kp1 + i) * 2 + 0] = tt.t[t][i][0];
+                htab[(static_cast<size_t>(t) * kp1 + i) * 2 + 1] = tt.t[t][i][1];
             }
+        for (int j = 0; j < L; ++j) {
+            hfull[2 * static_cast<size_t>(j)] = tt.t[0][j][0];
+            hfull[2 * static_cast<size_t>(j) + 1] = tt.t[0][j][1];
+        }
+        for (int j = 0; j < kp1; ++j) {  // a skew flip at half index j toggles j and L-1-j
+            uint64_t m = tt.t[0][j][0] ^ tt.t[0][j][1];
+            if (L - 1 - j != j) m ^= tt.t[0][L - 1 - j][0] ^ tt.t[0][L - 1 - j][1];
+            hfm[2 * static_cast<size_t>(kp1) + j] = m;
+        }
         fm.reserve(hfm.size());
         tab.reserve(htab.size());
+        tabfull.reserve(hfull.size());
         LABS_CUDA(cudaMemcpyAsync(fm.p, hfm.data(), hfm.size() * 8, cudaMemcpyHostToDevice, st));
         LABS_CUDA(cudaMemcpyAsync(tab.p, htab.data(), htab.size() * 8, cudaMemcpyHostToDevice, st));
+        LABS_CUDA(cudaMemcpyAsync(tabfull.p, hfull.data(), hfull.size() * 8, cudaMemcpyHostToDevice, st));
+        LABS_CUDA(cudaStreamSynchronize(st));  // host staging vectors die at scope end
         wp.fm = fm.p;
         wp.tab = tab.p;
-        wp.salt0 = tt.salt[0][wp.kp1];
-        wp.salt1 = tt.salt[1][wp.kp1];
+        wp.tabfull = tabfull.p;
+        wp.salt0 = tt.salt[0][kp1];
+        wp.salt1 = tt.salt[1][kp1];
+        wp.salt_full = tt.salt[0][L];
         int sms = 0;
         LABS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int bps = std::max(1, walk_blocks_per_sm(wp));
@@ -267,20 +284,31 @@ std::string walk_params_for(const Derived& d, bool count_visited, bool debug, Wa
     return err;
 }
 
-// Sort record views of a batch by (walk, iteration) with a counting pass over walks.
-std::vector<std::vector<WalkRecordView>> group_records(const BatchOut& b, int rec_words,
-                                                       int64_t nwalks) {
-    std::vector<std::vector<WalkRecordView>> by_walk(static_cast<size_t>(nwalks));
+// Record views of a batch sorted by (walk, iteration); `start[w]..start[w+1]` indexes walk w.
+struct GroupedRecords {
+    std::vector<WalkRecordView> recs;
+    std::vector<int64_t> start;
+    const WalkRecordView* begin(int64_t w) const { return recs.data() + start[static_cast<size_t>(w)]; }
+    const WalkRecordView* end(int64_t w) const { return recs.data() + start[static_cast<size_t>(w) + 1]; }
+};
+
+GroupedRecords group_records(const BatchOut& b, int rec_words, int64_t nwalks) {
+    GroupedRecords g;
+    g.recs.resize(static_cast<size_t>(b.nrec));
+    g.start.assign(static_cast<size_t>(nwalks) + 1, 0);
     for (int64_t i = 0; i < b.nrec; ++i) {
         const uint32_t* r = &b.rec[static_cast<size_t>(i) * rec_words];
-        WalkRecordView v{static_cast<int64_t>(r[0]), static_cast<int64_t>(r[1]),
-                         static_cast<int64_t>(static_cast<int32_t>(r[2])), r + kRecHeader};
-        by_walk[static_cast<size_t>(v.walk)].push_back(v);
+        g.recs[static_cast<size_t>(i)] = WalkRecordView{
+            static_cast<int64_t>(r[0]), static_cast<int64_t>(r[1]),
+            static_cast<int64_t>(static_cast<int32_t>(r[2])),
+            static_cast<uint64_t>(r[4]) | (static_cast<uint64_t>(r[5]) << 32), r + kRecHeader};
+        ++g.start[static_cast<size_t>(r[0]) + 1];
     }
-    for (auto& vv : by_walk)
-        std::sort(vv.begin(), vv.end(),
-                  [](const WalkRecordView& a, const WalkRecordView& c) { return a.iteration < c.iteration; });
-    return by_walk;
+    std::sort(g.recs.begin(), g.recs.end(), [](const WalkRecordView& a, const WalkRecordView& c) {
+        return a.walk != c.walk ? a.walk < c.walk : a.iteration < c.iteration;
+    });
+    for (int64_t w = 0; w < nwalks; ++w) g.start[static_cast<size_t>(w) + 1] += g.start[static_cast<size_t>(w)];
+    return g;
 }
 
 void half_bits_to_signs(const uint32_t* bits, int kp1, int8_t* half) {
@@ -288,23 +316,27 @@ void half_bits_to_signs(const uint32_t* bits, int kp1, int8_t* half) {
 }
 
 // Host replay of one walk's sieve hits: DedupSink -> CountingSink -> user sink.
+// Dedup uses the device-computed canonical_hash(0); only delivered candidates are expanded.
+// Delivery is per candidate (`emit`) or in batches (`emit_batch`, flushed every kBatch).
 struct SinkChain {
+    static constexpr int kBatch = 8192;
     const labs_saw_config* cfg;
     const Derived* d;
     labs_candidate_fn emit;
+    labs_candidate_batch_fn emit_batch;
     void* user;
     std::unordered_set<uint64_t> seen;
     int64_t emitted = 0;
     bool stop = false;
     bool aborted = false;
     std::vector<int8_t> half, full;
+    // pending batch
+    std::vector<int8_t> b_signs;
+    std::vector<int64_t> b_energy, b_walker, b_restart, b_iter;
+    std::vector<int32_t> b_class;
 
     void deliver(uint32_t walker, int64_t restart, const WalkRecordView& r) {
-        half.resize(static_cast<size_t>(d->kp1));
-        full.resize(static_cast<size_t>(d->L));
-        half_bits_to_signs(r.half, d->kp1, half.data());
-        expand_skew(half.data(), d->kp1, full.data());
-        if (!seen.insert(TabTables::get().hash(full.data(), d->L, 0)).second) return;
+        if (!seen.insert(r.hash).second) return;
         const int64_t n = ++emitted;
         if (cfg->candidate_quota > 0) {
             if (n > cfg->candidate_quota) {
@@ -314,13 +346,32 @@ struct SinkChain {
             }
             if (n >= cfg->candidate_quota) stop = true;
         }
-        if (emit && !aborted) {
+        if (aborted) return;
+        const int cls = static_cast<int>(walker % static_cast<uint32_t>(d->nprefix));
+        if (emit_batch) {
+            const size_t off = b_signs.size();
+            b_signs.resize(off + static_cast<size_t>(d->L));
+            half.resize(static_cast<size_t>(d->kp1));
+            half_bits_to_signs(r.half, d->kp1, half.data());
+            expand_skew(half.data(), d->kp1, b_signs.data() + off);
+            b_energy.push_back(r.energy);
+            b_walker.push_back(walker);
+            b_restart.push_back(restart);
+            b_iter.push_back(r.iteration);
+            b_class.push_back(cls);
+            if (static_cast<int>(b_energy.size()) >= kBatch) flush();
+            return;
+        }
+        if (emit) {
+            half.resize(static_cast<size_t>(d->kp1));
+            full.resize(static_cast<size_t>(d->L));
+            half_bits_to_signs(r.half, d->kp1, half.data());
+            expand_skew(half.data(), d->kp1, full.data());
             labs_candidate c{};
             c.length = d->L;
             c.origin = 0;
             c.energy = r.energy;
             c.signs = full.data();
-            const int cls = static_cast<int>(walker % static_cast<uint32_t>(d->nprefix));
             c.prefix = d->p > 0 ? &d->prefixes[static_cast<size_t>(cls) * d->p] : nullptr;
             c.prefix_len = d->p;
             c.walker = walker;
@@ -328,6 +379,29 @@ struct SinkChain {
             c.iteration = r.iteration;
             if (emit(user, &c) != 0) aborted = true;
         }
+    }
+
+    void flush() {
+        if (!emit_batch || b_energy.empty() || aborted) return;
+        labs_candidate_batch b{};
+        b.count = static_cast<int32_t>(b_energy.size());
+        b.length = d->L;
+        b.prefix_len = d->p;
+        b.origin = 0;
+        b.signs = b_signs.data();
+        b.energy = b_energy.data();
+        b.walker = b_walker.data();
+        b.restart = b_restart.data();
+        b.iteration = b_iter.data();
+        b.prefix_class = b_class.data();
+        b.prefixes = d->p > 0 ? d->prefixes.data() : nullptr;
+        if (emit_batch(user, &b) != 0) aborted = true;
+        b_signs.clear();
+        b_energy.clear();
+        b_walker.clear();
+        b_restart.clear();
+        b_iter.clear();
+        b_class.clear();
     }
 };
 
@@ -353,8 +427,8 @@ std::vector<uint32_t> walker_list(const labs_saw_config& cfg, const Derived& d, 
 
 constexpr int64_t kMaxBatchWalks = 1 << 20;
 
-int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
-             labs_pool_stats* out) {
+int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_batch_fn emit_batch,
+             void* user, labs_pool_stats* out) {
     const auto t0 = std::chrono::steady_clock::now();
     Derived d;
     std::string err = derive(cfg, d);
@@ -386,7 +460,12 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
                          cfg.time_budget_s > 0 || cfg.max_restarts == 0;
 
     PoolAccum acc;
-    SinkChain sink{&cfg, &d, emit, user, {}, 0, false, false, {}, {}};
+    SinkChain sink{};
+    sink.cfg = &cfg;
+    sink.d = &d;
+    sink.emit = emit;
+    sink.emit_batch = emit_batch;
+    sink.user = user;
     std::vector<std::unique_ptr<DeviceRunner>> runners;
     try {
         for (int g = 0; g < (coupled ? 1 : ngpu); ++g) {
@@ -406,8 +485,8 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
             const auto groups = group_records(b, wp.rec_words, nw);
             for (int64_t i = 0; i < nw && !sink.stop && !sink.aborted; ++i) {
                 const int64_t* s = &b.stats[static_cast<size_t>(i) * kWalkStatWords];
-                for (const auto& r : groups[static_cast<size_t>(i)])
-                    sink.deliver(static_cast<uint32_t>(b.walk_walker[i]), b.walk_restart[i], r);
+                for (const WalkRecordView* r = groups.begin(i); r != groups.end(i); ++r)
+                    sink.deliver(static_cast<uint32_t>(b.walk_walker[i]), b.walk_restart[i], *r);
                 ++acc.st.walks;
                 acc.st.iterations += s[kWsIterations];
                 acc.st.emitted_raw += s[kWsEmitted];
@@ -522,7 +601,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
                     int64_t i;
                 };
                 std::vector<Ref> refs;
-                std::vector<std::vector<std::vector<std::vector<WalkRecordView>>>> grp(static_cast<size_t>(ngpu));
+                std::vector<std::vector<GroupedRecords>> grp(static_cast<size_t>(ngpu));
                 for (int g = 0; g < ngpu; ++g)
                     for (size_t bi = 0; bi < outs[static_cast<size_t>(g)].size(); ++bi) {
                         const BatchOut& b = outs[static_cast<size_t>(g)][bi];
@@ -538,8 +617,9 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
                 for (const Ref& r : refs) {
                     const BatchOut& b = outs[static_cast<size_t>(r.g)][r.b];
                     const int64_t* s = &b.stats[static_cast<size_t>(r.i) * kWalkStatWords];
-                    for (const auto& v : grp[static_cast<size_t>(r.g)][r.b][static_cast<size_t>(r.i)])
-                        sink.deliver(r.walker, r.restart, v);
+                    const GroupedRecords& gr = grp[static_cast<size_t>(r.g)][r.b];
+                    for (const WalkRecordView* v = gr.begin(r.i); v != gr.end(r.i); ++v)
+                        sink.deliver(r.walker, r.restart, *v);
                     ++acc.st.walks;
                     acc.st.iterations += s[kWsIterations];
                     acc.st.emitted_raw += s[kWsEmitted];
@@ -615,6 +695,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, void* user,
         set_error("saw walk energy bookkeeping diverged");
         return LABS_ELOGIC;
     }
+    sink.flush();
     acc.st.emitted = sink.emitted;
     acc.st.best_energy = acc.best_set ? acc.st.best_energy : 0;
     acc.st.delta_evals = cfg.count_visited ? acc.st.delta_evals : -1;
@@ -712,9 +793,9 @@ int walks_from_halves(int L, int p, int64_t t_i, int64_t e_l, double fpr, const 
                 r.diverged = s[kWsDiverged];
             }
             if (on_rec)
-                for (const auto& v : groups[static_cast<size_t>(w)]) {
-                    half_bits_to_signs(v.half, kp1, half.data());
-                    if (on_rec(user, w, v.iteration, v.energy, half.data(), kp1) != 0) return LABS_EABORT;
+                for (const WalkRecordView* v = groups.begin(w); v != groups.end(w); ++v) {
+                    half_bits_to_signs(v->half, kp1, half.data());
+                    if (on_rec(user, w, v->iteration, v->energy, half.data(), kp1) != 0) return LABS_EABORT;
                 }
         }
     } catch (const CudaFailure& e) {
@@ -817,7 +898,16 @@ int labs_saw_pool_run(const labs_saw_config* cfg, labs_candidate_fn emit, void* 
         set_error("null config");
         return LABS_EINVAL;
     }
-    return pool_run(*cfg, emit, user, stats);
+    return pool_run(*cfg, emit, nullptr, user, stats);
+}
+
+int labs_saw_pool_run_batched(const labs_saw_config* cfg, labs_candidate_batch_fn emit, void* user,
+                              labs_pool_stats* stats) {
+    if (!cfg) {
+        set_error("null config");
+        return LABS_EINVAL;
+    }
+    return pool_run(*cfg, nullptr, emit, user, stats);
 }
 
 int labs_saw_walks(int32_t length, int32_t prefix_len, int64_t iterations,
@@ -913,12 +1003,9 @@ int labs_bench_run(labs_bench_plan* plan, int32_t reps, double* ms_per_rep, labs
             }
             // post-dedup count of the last rep's sieve hits
             std::unordered_set<uint64_t> seen;
-            std::vector<int8_t> half(static_cast<size_t>(bp.d.kp1)), full(static_cast<size_t>(bp.d.L));
             for (int64_t i = 0; i < b.nrec; ++i) {
                 const uint32_t* rr = &b.rec[static_cast<size_t>(i) * dr.wp.rec_words];
-                half_bits_to_signs(rr + kRecHeader, bp.d.kp1, half.data());
-                expand_skew(half.data(), bp.d.kp1, full.data());
-                seen.insert(TabTables::get().hash(full.data(), bp.d.L, 0));
+                seen.insert(static_cast<uint64_t>(rr[4]) | (static_cast<uint64_t>(rr[5]) << 32));
             }
             st.emitted = static_cast<int64_t>(seen.size());
             st.delta_evals = bp.cfg.count_visited ? st.delta_evals : -1;

@@ -210,7 +210,8 @@ std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bl
     wp.off_half = wp.off_dc + round_up(wp.S + 1, 4);
     wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
     wp.warp_words = wp.off_bloom + wp.bloom_words;
-    const int fm_words = round_up(2 * wp.kp1 * 2, 4);
+    const int fm_words = round_up(3 * wp.kp1 * 2, 4);
+    wp.fm_words = fm_words;
     int wpb = 4;
     while (wpb > 1 && (fm_words + wpb * wp.warp_words) * 4 > 227 * 1024) --wpb;
     if ((fm_words + wpb * wp.warp_words) * 4 > 227 * 1024)

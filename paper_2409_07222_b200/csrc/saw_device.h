@@ -7,7 +7,8 @@ namespace labs_b200 {
 
 constexpr int kMaxR = 16;          // neighbours per lane: free bits <= 32*16 = 512
 constexpr int kMaxHalf = 1024;     // TabulationHash::kMaxLen (rng.hpp:77)
-constexpr int kRecHeader = 4;      // record header words: walk, iteration, energy, flags
+constexpr int kRecHeader = 6;      // record header: walk, iteration, energy, flags,
+                                   // canonical_hash(0) of the full sequence (lo, hi)
 
 // Derived, device-ready description of one Step-1 launch (one batch of walks).
 // Per-walk shared-memory layout (32-bit word offsets inside a warp's slice):
@@ -41,9 +42,14 @@ struct WalkParams {
     int64_t nwalks;                // walks in this launch
     int64_t rec_cap;               // record slots in rec
     // inputs (device pointers)
-    const uint64_t* fm;            // [2][kp1] tabulation flip masks
-    const uint64_t* tab;           // [2][kp1][2] tabulation entries
+    const uint64_t* fm;            // [3][kp1]: tabulation flip masks of half position j in
+                                   //   tables 0/1 (Bloom keys), then the flip mask of the
+                                   //   full-sequence hash t0[j]^t0[L-1-j] (dedup key)
+    const uint64_t* tab;           // [2][kp1][2] tabulation entries (half hashes)
+    const uint64_t* tabfull;       // [L][2] table-0 entries of full positions (dedup key)
     uint64_t salt0, salt1;         // length salts for kp1
+    uint64_t salt_full;            // table-0 salt for L
+    int32_t fm_words;              // u32 words of the block-level fm table in shared memory
     const uint32_t* halves;        // [nwalks][hw] initial half bits (bit i set <=> +1)
     // outputs
     uint32_t* rec;                 // [rec_cap][rec_words]

@@ -71,8 +71,7 @@ __global__ void saw_seed_kernel(SeedParams P) {
 // ---------------------------------------------------------------------------
 // host-side launchers (called from the C++ orchestration)
 size_t walk_smem_bytes(const WalkParams& P) {
-    const int fm_words = ((2 * P.kp1 * 2) + 3) & ~3;
-    return (size_t)(fm_words + P.warps_per_block * P.warp_words) * 4;
+    return (size_t)(P.fm_words + P.warps_per_block * P.warp_words) * 4;
 }
 
 cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int* score_out,

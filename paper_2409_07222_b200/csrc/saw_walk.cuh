@@ -229,8 +229,8 @@ struct LagWords {  // lag words a lane may own: s = lane + 32 jj, S <= 4*ceil((3
 // dc bytes the C update publishes); the exact even-lag C live in the lag owners' registers.
 template <int R, bool COUNT>
 __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint64_t* fm0,
-                              const uint64_t* fm1, int64_t walk, int lane, int* score_out,
-                              int* corr_out) {
+                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, int lane,
+                              int* score_out, int* corr_out) {
     constexpr int NJ = LagWords<R>::value;
     const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
     const int nj = (S + 31) >> 5;  // lag words owned per lane (<= NJ)
@@ -347,6 +347,13 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     }
     h1 ^= P.salt0;
     h2 ^= P.salt1;
+    // canonical_hash(0) of the full expanded sequence (DedupSink key, candidate.hpp:84-99,
+    // rng.hpp:89-95), kept incrementally: a skew flip at j toggles positions j and L-1-j
+    uint64_t hf = 0;
+    for (int j = lane; j < L; j += 32) hf ^= P.tabfull[2 * j + (x_of_half(w.half, k, j) > 0)];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hf ^= shfl_xor64(hf, o);
+    hf ^= P.salt_full;
     if (lane < P.bloom_k) {
         const uint32_t idx = bloom_index(h1, h2, lane, P.bloom_mu, P.bloom_bits);
         atomicOr(&w.bloom[idx >> 5], 1u << (idx & 31));
@@ -579,6 +586,7 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
         }
         h1 ^= fm0[astar];
         h2 ^= fm1[astar];
+        hf ^= fmf[astar];
         if (lane < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
         energy += dstar;
         best = min(best, energy);
@@ -595,6 +603,8 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                     r[1] = (uint32_t)(it + 1);
                     r[2] = (uint32_t)energy;
                     r[3] = 0;
+                    r[4] = (uint32_t)hf;
+                    r[5] = (uint32_t)(hf >> 32);
                 }
                 for (int i = lane; i < P.hw; i += 32) r[kRecHeader + i] = w.half[i];
             }
@@ -624,9 +634,9 @@ __global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkPara
                                                                         int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
-    for (int i = threadIdx.x; i < 2 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
+    for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
     __syncthreads();
-    const int fm_words = ((2 * P.kp1 * 2) + 3) & ~3;  // u32 words, 16-byte aligned
+    const int fm_words = P.fm_words;  // u32 words, 16-byte aligned
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + fm_words + warp * P.warp_words;
     WarpSmem w;
@@ -644,7 +654,8 @@ __global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkPara
     const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
     for (int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp; walk < P.nwalks;
          walk += stride)
-        run_walk_warp<R, COUNT>(P, w, fm, fm + P.kp1, walk, lane, score_out, corr_out);
+        run_walk_warp<R, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, lane, score_out,
+                                corr_out);
 }
 
 // Per-R launch / occupancy helpers, explicitly instantiated in saw_walk_r*.cu so that
