@@ -17,69 +17,14 @@
 #include <thread>
 #include <vector>
 
+#include "cli_args.hpp"
 #include "labs_b200.hpp"
 
 namespace {
-
-int default_threads() {  // labs_main.cpp:21-28
-    if (const char* env = std::getenv("LABS_THREADS")) {
-        const int n = std::atoi(env);
-        if (n >= 1) return n;
-    }
-    const unsigned hc = std::thread::hardware_concurrency();
-    return hc ? static_cast<int>(hc) : 1;
-}
-
-// Minimal CLI11-compatible option parsing: --opt v, --opt=v, -L v, -Lv, flags.
-class Args {
-public:
-    Args(int argc, char** argv, int first) {
-        for (int i = first; i < argc; ++i) toks_.emplace_back(argv[i]);
-    }
-    // returns false and sets error on malformed input
-    bool parse(const std::map<std::string, std::string*>& opts,
-               const std::map<std::string, bool*>& flags, std::string& err) {
-        for (size_t i = 0; i < toks_.size(); ++i) {
-            std::string t = toks_[i], val;
-            bool has_val = false;
-            if (t.rfind("--", 0) == 0) {
-                const auto eq = t.find('=');
-                if (eq != std::string::npos) {
-                    val = t.substr(eq + 1);
-                    t = t.substr(0, eq);
-                    has_val = true;
-                }
-            } else if (t.size() > 2 && t[0] == '-' && t[1] != '-') {
-                val = t.substr(2);
-                if (!val.empty() && val[0] == '=') val = val.substr(1);
-                t = t.substr(0, 2);
-                has_val = true;
-            }
-            auto f = flags.find(t);
-            if (f != flags.end()) {
-                *f->second = true;
-                continue;
-            }
-            auto o = opts.find(t);
-            if (o == opts.end()) {
-                err = "The following argument was not expected: " + toks_[i];
-                return false;
-            }
-            if (!has_val) {
-                if (i + 1 >= toks_.size()) {
-                    err = t + " requires an argument";
-                    return false;
-                }
-                val = toks_[++i];
-            }
-            *o->second = val;
-        }
-        return true;
-    }
-
-private:
-    std::vector<std::string> toks_;
-};
+using labs_cli::Args;
+using labs_cli::default_threads;
+using labs_cli::to_d;
+using labs_cli::to_ll;
 
 class FileSink final : public labs_b200::CandidateSink {  // labs_main.cpp:30-43
 public:
@@ -91,19 +36,6 @@ public:
 private:
     std::ofstream out_;
 };
-
-long long to_ll(const std::string& s, const char* name) {
-    char* end = nullptr;
-    const long long v = std::strtoll(s.c_str(), &end, 10);
-    if (s.empty() || *end) throw std::invalid_argument(std::string(name) + ": not an integer: " + s);
-    return v;
-}
-double to_d(const std::string& s, const char* name) {
-    char* end = nullptr;
-    const double v = std::strtod(s.c_str(), &end);
-    if (s.empty() || *end) throw std::invalid_argument(std::string(name) + ": not a number: " + s);
-    return v;
-}
 
 int cmd_saw(int argc, char** argv) {
     labs_b200::SawConfig saw;
