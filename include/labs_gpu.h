@@ -175,6 +175,18 @@ int labs_enumerate_class(int32_t length, int32_t prefix_len, int32_t class_index
                          int64_t energy_threshold, uint64_t g_begin, uint64_t g_end,
                          labs_enum_fn emit, void* user, labs_enum_stats* stats);
 
+/* K5, Step-2 neighbourhood scoring: everything refine
+ * (pq.cpp:114-176) computes for one pivot, exactly, in one launch:
+ *   deltas[i]                     flip_delta(pivot, i)                 (sequence.cpp:42-58)
+ *   rot_energy[(i*2+dir)*t_r+r-1] energy of neighbour i after r one-step rotations,
+ *                                 dir 0 = left, 1 = right              (pq.cpp:56-101)
+ *   rot_hash[same index]          canonical_hash(0) of that sequence   (rng.hpp:89-95)
+ *   *pivot_energy                 E(pivot)
+ * The caller replays the frontier (seen / mark / push) in the reference order.
+ * Thread-safe: each host thread uses its own stream and buffers. */
+int labs_pq_score(int32_t length, int32_t t_r, const int8_t* pivot, int32_t* deltas,
+                  int32_t* rot_energy, uint64_t* rot_hash, int64_t* pivot_energy);
+
 /* Device-resident benchmark plan: the whole pool's walks with inputs in HBM.
  * labs_bench_run times `reps` launches (seed + walk kernels) with CUDA events on the
  * library's stream; before every rep (outside the timed events) a 256 MiB scratch

@@ -213,6 +213,11 @@ class Restated(_Base):
         c, _ = self.correlations(a)
         return self.lib.lo_skew_flip_delta_fast(p, len(a), c.ctypes.data_as(C.POINTER(C.c_int64)), hp)
 
+    def flip_delta(self, s, i):
+        a, p = _i8(s)
+        c, _ = self.correlations(a)
+        return self.lib.lo_flip_delta(p, len(a), c.ctypes.data_as(C.POINTER(C.c_int64)), i)
+
     def apply_skew_flip(self, s, hp):
         a, p = _i8(np.array(s, dtype=np.int8).copy())
         c, e = self.correlations(a)

@@ -151,6 +151,9 @@ def load_library():
         lib.labs_bench_run.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(_PoolStats)]
         lib.labs_bench_destroy.argtypes = [C.c_void_p]
+        lib.labs_pq_score.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int8),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
         lib.labs_int32_peak.argtypes = [C.POINTER(C.c_double)] * 4 + [C.POINTER(C.c_int32)] * 2
         lib.labs_device_count.argtypes = [C.POINTER(C.c_int32)]
         lib.labs_canonical_hash.restype = C.c_uint64
@@ -477,6 +480,25 @@ def enumerate_class(length: int, prefix_len: int, class_index: int, m: int,
     _check(lib.labs_enumerate_class(length, prefix_len, class_index, m, energy_threshold,
                                     g_begin, g_end, cb, None, C.byref(st)))
     return hits, {n: getattr(st, n) for n, _ in _EnumStats._fields_}
+
+
+def pq_score(pivot, t_r: int):
+    """K5: Step-2 neighbourhood scores of one refine pivot (pq.cpp:114-176) on the GPU.
+
+    Returns (pivot_energy, deltas [L], rot_energy [L, 2, t_r], rot_hash [L, 2, t_r]) where
+    deltas[i] = flip_delta(pivot, i) and rot_*[i, dir, r-1] describe neighbour i rotated
+    r steps left (dir 0) / right (dir 1)."""
+    lib = load_library()
+    a, p = _i8(pivot)
+    n = len(a)
+    d = np.zeros(n, dtype=np.int32)
+    re = np.zeros((n, 2, max(t_r, 1)), dtype=np.int32)
+    rh = np.zeros((n, 2, max(t_r, 1)), dtype=np.uint64)
+    e = C.c_int64()
+    _check(lib.labs_pq_score(n, t_r, p, d.ctypes.data_as(C.POINTER(C.c_int32)),
+                             re.ctypes.data_as(C.POINTER(C.c_int32)),
+                             rh.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(e)))
+    return e.value, d, re[:, :, :t_r], rh[:, :, :t_r]
 
 
 class bench_plan:

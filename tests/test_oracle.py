@@ -218,3 +218,15 @@ def test_enumeration_restatement(restated):
         best = min(restated.enumerate_class(L, p, c, kp1 - p, 1)[1]["best_energy"]
                    for c in range(1 << (p - 1)))
         assert best == restated.oracle_skew_exhaustive(L)[0]
+
+
+def test_flip_delta_equals_scratch(restated):
+    # test_sequence.cpp:83-98: flip_delta = scratch at L in {50, 101, 250}, seed 42
+    rng = np.random.default_rng(42)
+    for L in (50, 101, 250):
+        s = _rand_signs(rng, L)
+        e0 = _scratch_energy(s)
+        for i in rng.integers(0, L, size=6):
+            t = s.copy()
+            t[i] = -t[i]
+            assert restated.flip_delta(s, int(i)) == _scratch_energy(t) - e0
