@@ -91,12 +91,8 @@ RefineResult refine(const Candidate& start, const PqConfig& config) {
                     const std::uint64_t hr = rot_h[o];
                     if (frontier.seen(hr)) continue;
                     frontier.mark(hr);
-                    const Sign* x = seq.data();
-                    for (int j = 0; j < n; ++j) {  // left: v_j = x_{j+r}; right: v_j = x_{j-r}
-                        int src = dir == 0 ? j + r : j - r;
-                        src = ((src % n) + n) % n;
-                        rot[static_cast<std::size_t>(j)] = x[src];
-                    }
+                    const Sign* x = seq.data();  // left: v_j = x_{j+r}; right: v_j = x_{j-r}
+                    std::rotate_copy(x, x + (dir == 0 ? r : n - r), x + n, rot.begin());
                     frontier.push(BinarySequence(rot), rot_e[o]);
                 }
             }
