@@ -271,6 +271,42 @@ public:
     }
 };
 
+// Device contexts (stream, events, uploaded hash tables, grow-only batch buffers) are kept
+// across run_saw_pool calls with the same walk geometry, so a call pays no allocation or
+// table upload when the configuration repeats (the pipeline calls Step 1 once per round).
+// (heap-allocated and never destroyed: no CUDA calls from static destructors at exit)
+std::mutex g_runner_mu;
+std::vector<std::unique_ptr<DeviceRunner>>& g_runner_pool = *new std::vector<std::unique_ptr<DeviceRunner>>();
+
+bool same_geometry(const WalkParams& a, const WalkParams& b) {
+    return a.L == b.L && a.p == b.p && a.t_i == b.t_i && a.bloom_bits == b.bloom_bits &&
+           a.bloom_k == b.bloom_k && a.count_visited == b.count_visited &&
+           a.debug_check == b.debug_check;
+}
+
+std::unique_ptr<DeviceRunner> acquire_runner(int dev, const WalkParams& wp) {
+    {
+        std::lock_guard<std::mutex> lock(g_runner_mu);
+        for (size_t i = 0; i < g_runner_pool.size(); ++i)
+            if (g_runner_pool[i]->dev == dev && same_geometry(g_runner_pool[i]->wp, wp)) {
+                std::unique_ptr<DeviceRunner> r = std::move(g_runner_pool[i]);
+                g_runner_pool.erase(g_runner_pool.begin() + static_cast<long>(i));
+                r->wp.e_l = wp.e_l;
+                return r;
+            }
+    }
+    std::unique_ptr<DeviceRunner> r(new DeviceRunner());
+    r->init(dev, wp);
+    return r;
+}
+
+void release_runners(std::vector<std::unique_ptr<DeviceRunner>>& rs) {
+    std::lock_guard<std::mutex> lock(g_runner_mu);
+    for (auto& r : rs)
+        if (r && g_runner_pool.size() < 16) g_runner_pool.push_back(std::move(r));
+    rs.clear();
+}
+
 int device_count() {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -468,10 +504,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
     sink.user = user;
     std::vector<std::unique_ptr<DeviceRunner>> runners;
     try {
-        for (int g = 0; g < (coupled ? 1 : ngpu); ++g) {
-            runners.emplace_back(new DeviceRunner());
-            runners.back()->init(first + g, wp);
-        }
+        for (int g = 0; g < (coupled ? 1 : ngpu); ++g) runners.push_back(acquire_runner(first + g, wp));
         // ---- build the ordered walk sequence as batches of segments ----
         // Per walker: state carried across batches (only in coupled mode can a walker's
         // restarts span batches).
@@ -686,11 +719,12 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
         }
     } catch (const CudaFailure& e) {
         set_error(e.what());
-        return LABS_ECUDA;
+        return LABS_ECUDA;  // runners dropped: their state may be unusable
     } catch (const std::bad_alloc&) {
         set_error("out of host memory");
         return LABS_ECUDA;
     }
+    release_runners(runners);
     if (acc.diverged) {
         set_error("saw walk energy bookkeeping diverged");
         return LABS_ELOGIC;
