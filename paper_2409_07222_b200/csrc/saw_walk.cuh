@@ -626,11 +626,16 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     __syncwarp();
 }
 
-#ifndef LABS_MIN_BLOCKS
-#define LABS_MIN_BLOCKS 4
-#endif
+// Resident 128-thread blocks per SM the register allocation is sized for: 4 (<= 128
+// registers) up to R = 8; wider lanes (R neighbours each) get more registers instead of
+// spilling (R = 16 needs ~200).
+template <int R>
+struct MinBlocks {
+    static constexpr int value = R <= 8 ? 4 : (R <= 12 ? 3 : 2);
+};
+
 template <int R, bool COUNT>
-__global__ void __launch_bounds__(128, LABS_MIN_BLOCKS) saw_walk_kernel(WalkParams P, int* score_out,
+__global__ void __launch_bounds__(128, MinBlocks<R>::value) saw_walk_kernel(WalkParams P, int* score_out,
                                                                         int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
