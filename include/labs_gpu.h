@@ -50,7 +50,8 @@ typedef struct labs_saw_config {
     int64_t stop_at_energy;
     int32_t debug_check_energy;
     /* --- additive GPU controls --- */
-    int32_t n_gpus;            /* devices used by this call (0 or 1 = one) */
+    int32_t n_gpus;            /* class shards run concurrently, shard g on device (device + g)
+                                  mod the devices available; 0 or 1 = one */
     int32_t device;            /* first device ordinal */
     int32_t shard_index;       /* restriction-class shard of this process: walkers with */
     int32_t shard_count;       /*   (w mod 2^(p-1)) mod shard_count == shard_index      */

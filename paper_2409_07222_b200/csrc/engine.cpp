@@ -484,7 +484,10 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
         return LABS_ENODEV;
     }
     const int first = std::max(0, cfg.device);
-    const int ngpu = std::max(1, std::min(cfg.n_gpus > 0 ? cfg.n_gpus : 1, ndev_avail - first));
+    // n_gpus class shards run concurrently, shard g on device first + g (mod the devices
+    // available from `first`); more shards than devices share a device (separate streams)
+    const int ngpu = std::max(1, cfg.n_gpus);
+    const int ndev_use = std::max(1, ndev_avail - first);
     if (first >= ndev_avail) {
         set_error("device ordinal out of range");
         return LABS_ENODEV;
@@ -504,7 +507,8 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
     sink.user = user;
     std::vector<std::unique_ptr<DeviceRunner>> runners;
     try {
-        for (int g = 0; g < (coupled ? 1 : ngpu); ++g) runners.push_back(acquire_runner(first + g, wp));
+        for (int g = 0; g < (coupled ? 1 : ngpu); ++g)
+            runners.push_back(acquire_runner(first + g % ndev_use, wp));
         // ---- build the ordered walk sequence as batches of segments ----
         // Per walker: state carried across batches (only in coupled mode can a walker's
         // restarts span batches).
