@@ -239,7 +239,7 @@ public:
             P.rec_count = rec_count.p;
             P.walk_stats = stats.p;
             const int grid = static_cast<int>(std::max<int64_t>(
-                1, std::min<int64_t>(grid_cap, (nwalks + P.warps_per_block - 1) / P.warps_per_block)));
+                1, std::min<int64_t>(grid_cap, (nwalks + P.walks_per_block - 1) / P.walks_per_block)));
             LABS_CUDA(cudaMemsetAsync(rec_count.p, 0, sizeof(unsigned long long), st));
             LABS_CUDA(cudaEventRecord(ev[0], st));
             LABS_CUDA(launch_saw_walk(P, grid, st, score_out, corr_out));

@@ -36,6 +36,8 @@ struct WalkParams {
     int32_t warp_words;            // shared-memory words per walk (warp)
     int32_t off_x1, off_kl, off_kh, off_c16, off_kq, off_dc, off_half, off_bloom;  // X0 at 0
     int32_t warps_per_block;
+    int32_t lpw;                   // lanes per walk (32: one walk per warp; 16: two)
+    int32_t walks_per_block;       // warps_per_block * 32 / lpw
     int32_t debug_check;           // re-derive E from C every iteration, flag divergence
     int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)
     int32_t rec_words;             // kRecHeader + hw

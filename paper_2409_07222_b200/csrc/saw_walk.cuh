@@ -216,30 +216,90 @@ __device__ __forceinline__ void store_k_word(const WarpSmem& w, const WalkParams
     }
 }
 
-template <int R>
-struct LagWords {  // lag words a lane may own: s = lane + 32 jj, S <= 4*ceil((32R+29)/128)*32
-    static constexpr int value = (32 * R + 29 + 127) / 128 < 4 ? (32 * R + 29 + 127) / 128 : 4;
+// ---------------------------------------------------------------------------
+// Segments: a warp runs 32 / LPW walks side by side, LPW lanes each (LPW = 32: one walk
+// per warp).  With LPW = 16 every warp-wide instruction of the per-step bookkeeping
+// (argmin, Bloom probe, apply) serves two walks and each lane owns 2x the neighbours, so
+// more walks share an SM's issue slots and latency.  All reductions stay inside a segment
+// (width-LPW shuffles); control flow is per segment with warp-uniform loops.
+template <int LPW>
+struct Seg {
+    static constexpr int kSegs = 32 / LPW;
+    static constexpr uint32_t kLow = LPW == 32 ? 0xffffffffu : ((1u << LPW) - 1u);
+    int lane, sl, base;
+    __device__ __forceinline__ explicit Seg(int l) : lane(l), sl(l % LPW), base(l - l % LPW) {}
+    __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o, LPW);
+        return v;
+    }
+    __device__ __forceinline__ long long sum64(long long v) const {
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v += (long long)shfl_xor64((uint64_t)v, o);
+        return v;
+    }
+    __device__ __forceinline__ uint64_t xor64(uint64_t v) const {
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v ^= shfl_xor64(v, o);
+        return v;
+    }
+    __device__ __forceinline__ uint32_t umin(uint32_t v) const {
+        if (LPW == 32) return __reduce_min_sync(FULLMASK, v);
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o, LPW));
+        return v;
+    }
+    __device__ __forceinline__ int imin(int v) const {
+        if (LPW == 32) return __reduce_min_sync(FULLMASK, v);
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o, LPW));
+        return v;
+    }
+    __device__ __forceinline__ bool all(bool b) const {
+        if (LPW == 32) return __all_sync(FULLMASK, b);
+        return ((__ballot_sync(FULLMASK, b) >> base) & kLow) == kLow;
+    }
+    __device__ __forceinline__ bool any(bool b) const {
+        if (LPW == 32) return __any_sync(FULLMASK, b);
+        return ((__ballot_sync(FULLMASK, b) >> base) & kLow) != 0;
+    }
+    // "some segment of this warp has b" for a segment-uniform b (loop control); with one
+    // segment per warp b is already warp-uniform and needs no vote
+    __device__ __forceinline__ bool uni(bool b) const {
+        if (LPW == 32) return b;
+        return __any_sync(FULLMASK, b);
+    }
+    template <typename T>
+    __device__ __forceinline__ T bcast(T v) const { return __shfl_sync(FULLMASK, v, 0, LPW); }
 };
 
-// K1: one warp = one walk.  v3 bookkeeping: the per-neighbour constant part of the delta
+template <int R, int LPW>
+struct LagWords {  // lag words a lane may own: s = sl + LPW jj, S = ceil(k/4) <= 128
+    static constexpr int a = (LPW * R + 32 + 4 * LPW - 1) / (4 * LPW);
+    static constexpr int b = 128 / LPW;
+    static constexpr int value = a < b ? a : b;
+};
+
+// K1: LPW lanes = one walk.  The per-neighbour constant part of the delta
 //     T(a) = 16 N(a) + 32 Q(a) + 8 (-1)^(k-a) C_{2(k-a)}   (a < k),   4 N + 8 Q  (a = k)
 // and xs(a) = 8 x_a (4 x_k) live in the owning lane's registers, so a delta is one IMAD on
 // the sliding dot product G(a): dE(a) = T(a) - xs(a) G(a).  Per step T is updated in O(1)
 // per neighbour (Q pairs through the flipped positions, and the C term from the per-lag
 // dc bytes the C update publishes); the exact even-lag C live in the lag owners' registers.
-template <int R, bool COUNT>
-__device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint64_t* fm0,
-                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, int lane,
-                              int* score_out, int* corr_out) {
-    constexpr int NJ = LagWords<R>::value;
+template <int R, int LPW, bool COUNT>
+__device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint64_t* fm0,
+                             const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
+                             const Seg<LPW>& sg, int* score_out, int* corr_out) {
+    constexpr int NJ = LagWords<R, LPW>::value;
     const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
-    const int nj = (S + 31) >> 5;  // lag words owned per lane (<= NJ)
+    const int sl = sg.sl;
+    const int nj = (S + LPW - 1) / LPW;  // lag words owned per lane (<= NJ)
 
     // ---- load the initial half, build parity arrays, clear kernel + Bloom ----
-    const uint32_t* src = P.halves + walk * P.hw;
-    for (int i = lane; i < P.hw; i += 32) w.half[i] = src[i];
+    const uint32_t* src = P.halves + (valid ? walk : 0) * P.hw;
+    for (int i = sl; i < P.hw; i += LPW) w.half[i] = valid ? src[i] : 0u;
     __syncwarp();
-    for (int wi = lane; wi < 2 * P.xwords; wi += 32) {
+    for (int wi = sl; wi < 2 * P.xwords; wi += LPW) {
         const int par = wi >= P.xwords;
         const int word = wi - par * P.xwords;
         uint32_t v = 0;
@@ -252,11 +312,11 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
         }
         (par ? w.X1w : w.X0w)[word] = v;
     }
-    for (int i = lane; i < 2 * P.kwords; i += 32) w.KL[i] = 0;  // KL and KH are adjacent
-    if (lane == 0) w.DC[-1] = 0;  // dc of "lag 0" (the centre neighbour has no C term)
+    for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
+    if (sl == 0) w.DC[-1] = 0;  // dc of "lag 0" (the centre neighbour has no C term)
     {
         uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
-        for (int i = lane; i < (P.bloom_words >> 2); i += 32) b4[i] = make_uint4(0, 0, 0, 0);
+        for (int i = sl; i < (P.bloom_words >> 2); i += LPW) b4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
 
@@ -265,7 +325,7 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     int C[NJ][4];
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) {
-        const int s = lane + 32 * jj;
+        const int s = sl + LPW * jj;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int t = 4 * s + 1 + b;
@@ -276,24 +336,24 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
             cmax = max(cmax, abs(v));
         }
     }
-    int energy = warp_sum(e_part);
-    bool wide = __reduce_max_sync(FULLMASK, (unsigned)cmax) > 127u;
+    int energy = sg.sum(e_part);
+    bool wide = sg.any(cmax > 127);
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) {
-        const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1);
-        const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, 31);
-        const int s = lane + 32 * jj;
-        const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
+        const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1, LPW);
+        const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
+        const int s = sl + LPW * jj;
+        const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
         if (jj < nj && s < S) {
             store_c_word(w, P, s, C[jj], cprev, wide);
-            if (corr_out)
+            if (corr_out && valid)
                 for (int b = 0; b < 4; ++b)
                     if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = C[jj][b];
         }
     }
 
     // ---- 16N + 32Q per half index (lanes over a), once per walk ----
-    for (int a = P.p + lane; a <= k; a += 32) {
+    for (int a = P.p + sl; a <= k; a += LPW) {
         const int8_t* Xb = ((a & 1) ? w.X1 : w.X0) + P.xoff + (a >> 1);
         const int tstar = (a < k) ? (k - a) : -1;
         int q = 0;
@@ -305,7 +365,7 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     __syncwarp();
 
     // ---- lane geometry: this lane's neighbours a = a0 + 8m (all of parity `par`) ----
-    const int cgrp = lane & 7, g = lane >> 3;
+    const int cgrp = sl & 7, g = sl >> 3;
     const int a0 = P.p + cgrp + 8 * R * g;
     const int par = a0 & 1, a0h = a0 >> 1;
     const uint32_t* Xw = (par ? w.X1w : w.X0w) + (P.xoff >> 2);
@@ -335,27 +395,20 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
 
     // ---- half hashes h1, h2 (saw.cpp:77-89) and the initial Bloom insert ----
     uint64_t h1 = 0, h2 = 0;
-    for (int i = lane; i < kp1; i += 32) {
+    for (int i = sl; i < kp1; i += LPW) {
         const int bit = (w.half[i >> 5] >> (i & 31)) & 1;
         h1 ^= P.tab[(0 * kp1 + i) * 2 + bit];
         h2 ^= P.tab[(1 * kp1 + i) * 2 + bit];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        h1 ^= shfl_xor64(h1, o);
-        h2 ^= shfl_xor64(h2, o);
-    }
-    h1 ^= P.salt0;
-    h2 ^= P.salt1;
+    h1 = sg.xor64(h1) ^ P.salt0;
+    h2 = sg.xor64(h2) ^ P.salt1;
     // canonical_hash(0) of the full expanded sequence (DedupSink key, candidate.hpp:84-99,
     // rng.hpp:89-95), kept incrementally: a skew flip at j toggles positions j and L-1-j
     uint64_t hf = 0;
-    for (int j = lane; j < L; j += 32) hf ^= P.tabfull[2 * j + (x_of_half(w.half, k, j) > 0)];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) hf ^= shfl_xor64(hf, o);
-    hf ^= P.salt_full;
-    if (lane < P.bloom_k) {
-        const uint32_t idx = bloom_index(h1, h2, lane, P.bloom_mu, P.bloom_bits);
+    for (int j = sl; j < L; j += LPW) hf ^= P.tabfull[2 * j + (x_of_half(w.half, k, j) > 0)];
+    hf = sg.xor64(hf) ^ P.salt_full;
+    for (int i = sl; i < P.bloom_k; i += LPW) {
+        const uint32_t idx = bloom_index(h1, h2, i, P.bloom_mu, P.bloom_bits);
         atomicOr(&w.bloom[idx >> 5], 1u << (idx & 31));
     }
     __syncwarp();
@@ -373,16 +426,20 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
         if (a0 + 8 * m > k) inval |= 1u << m;
     uint32_t skip = inval;
     const int64_t t_i = score_out ? 1 : P.t_i;
+    const bool one_key = L <= 1001;
+    bool active = valid;  // this segment's walk is still running
 
-    for (long long it = 0; it < t_i; ++it) {
+    for (long long it = 0;; ++it) {
+        const bool cont = active && it < t_i;
+        if (!sg.uni(cont)) break;
         // ---- G for all owned neighbours (the O(L) part: IDP4A sliding dot product) ----
         int acc[R], acch[R];
-        if (wide) {
+        if (sg.uni(wide && cont)) {
             g_neighbours<R, true>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
-            ++wide_iters;
         } else {
             g_neighbours<R, false>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
         }
+        if (wide && cont) ++wide_iters;
         // ---- exact deltas: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
@@ -391,14 +448,15 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
             delta[m] = T[m] - xs[m] * gg;
         }
         if (score_out) {
+            if (valid)
 #pragma unroll
-            for (int m = 0; m < R; ++m)
-                if (a0 + 8 * m <= k) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
+                for (int m = 0; m < R; ++m)
+                    if (a0 + 8 * m <= k) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
             break;
         }
 
         // ---- choose: lowest (delta, hp) among unvisited (best_neighbour, saw.cpp:106-115) ----
-        if (COUNT) {
+        if (COUNT && cont) {
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 if (a0 + 8 * m > k) continue;  // in `inval`
@@ -419,19 +477,21 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
         // lane minimum, lowest m first; `skip` excludes the undo move (the previous pivot
         // is always in the filter) without a Bloom probe, and the non-neighbours a > k.
         // For L <= 1001, |dE| < 2^22 and one unsigned key (dE + 2^22) << 9 | a orders
-        // (delta, hp) lexicographically, so one REDUX finds the winner.
+        // (delta, hp) lexicographically, so one segment minimum finds the winner.
         int dstar = 0, astar = -1;
         uint32_t ins_idx = 0;  // Bloom bit of the accepted neighbour, reused for the insert
-        const bool one_key = L <= 1001;
         uint32_t bkey = 0xffffffffu;
         int bd = INT_BIG, bm = 0;
-        if (one_key) {
+        if (one_key) {  // pairwise (tree) minimum: log2(R) dependent steps, not R
+            uint32_t key[R];
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
-                const uint32_t key = (skip & (1u << m)) ? 0xffffffffu
-                                                        : (uint32_t)delta[m] * 512u + kbase + 8u * m;
-                bkey = min(bkey, key);
-            }
+            for (int m = 0; m < R; ++m)
+                key[m] = (skip & (1u << m)) ? 0xffffffffu : (uint32_t)delta[m] * 512u + kbase + 8u * m;
+#pragma unroll
+            for (int h = 1; h < R; h <<= 1)
+#pragma unroll
+                for (int m = 0; m + h < R; m += 2 * h) key[m] = min(key[m], key[m + h]);
+            bkey = key[0];
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m)
@@ -440,35 +500,45 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                     bm = m;
                 }
         }
-        while (true) {
+        bool need = cont;  // this segment still has to pick its neighbour
+        while (sg.uni(need)) {
             int md, ma;
             bool mine_won;
             if (one_key) {
-                const uint32_t k_best = __reduce_min_sync(FULLMASK, bkey);
-                if (k_best == 0xffffffffu) break;  // every free neighbour visited
+                const uint32_t k_best = sg.umin(bkey);
                 ma = (int)(k_best & 511u);
                 md = (int)(k_best >> 9) - (1 << 22);
                 mine_won = bkey == k_best;
+                if (k_best == 0xffffffffu) need = false;  // every free neighbour visited
             } else {
-                md = __reduce_min_sync(FULLMASK, bd);
-                if (md == INT_BIG) break;
+                md = sg.imin(bd);
                 const int mine = (bd == md) ? a0 + 8 * bm : INT_BIG;
-                ma = __reduce_min_sync(FULLMASK, mine);
+                ma = sg.imin(mine);
                 mine_won = mine == ma;
+                if (md == INT_BIG) need = false;
             }
-            const uint64_t n1 = h1 ^ fm0[ma], n2 = h2 ^ fm1[ma];
+            if (LPW == 32 && !need) break;  // (warp-uniform with one segment per warp)
+            const int mac = need ? ma : P.p;  // a safe index for segments not probing
+            const uint64_t n1 = h1 ^ fm0[mac], n2 = h2 ^ fm1[mac];
             bool bit = true;
-            if (lane < P.bloom_k) {
-                ins_idx = bloom_index(n1, n2, lane, P.bloom_mu, P.bloom_bits);
-                bit = (w.bloom[ins_idx >> 5] >> (ins_idx & 31)) & 1;
+            if (LPW >= 32 || sl < P.bloom_k) {  // one hash index per lane (bloom_k <= LPW)
+                const uint32_t idx = bloom_index(n1, n2, sl, P.bloom_mu, P.bloom_bits);
+                if (sl < P.bloom_k) {
+                    bit = (w.bloom[idx >> 5] >> (idx & 31)) & 1;
+                    if (need) ins_idx = idx;  // kept for the insert if accepted
+                }
             }
             if (COUNT) {  // already filtered: the minimum is unvisited
-                dstar = md;
-                astar = ma;
-                break;
+                if (need) {
+                    dstar = md;
+                    astar = ma;
+                }
+                need = false;
+                continue;
             }
-            ++probes;
-            if (__all_sync(FULLMASK, bit)) {
+            const bool visited = sg.all(bit);
+            if (need) ++probes;
+            if (need && visited) {
                 if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
                     skip |= 1u << ((ma - a0) >> 3);
                     bkey = 0xffffffffu;
@@ -484,58 +554,62 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                         }
                     }
                 }
-                continue;
+            } else if (need) {
+                dstar = md;
+                astar = ma;
+                need = false;
             }
-            dstar = md;
-            astar = ma;
-            break;
         }
-        if (astar < 0) {
+        if (cont && astar < 0) {
             exhausted = 1;
-            break;
+            active = false;
         }
+        const bool step = cont && astar >= 0;  // segment-uniform
 
         // ---- apply the skew flip at astar (apply_skew_flip, skew.cpp:95-105) ----
-        ++iterations;
-        const bool cen = astar == k;
-        const int bstar = L - 1 - astar;
-        const int apar = astar & 1, ah = astar >> 1;
+        if (step) ++iterations;
+        const int as = step ? astar : P.p;  // addresses stay in range for idle segments
+        const bool cen = as == k;
+        const int bstar = L - 1 - as;
+        const int apar = as & 1, ah = as >> 1;
         int8_t* Xa = (apar ? w.X1 : w.X0) + P.xoff;
         const int xa = Xa[ah];
-        const int xb = cen ? 0 : (((k - astar) & 1) ? -xa : xa);
-        const int dstar_l = astar - a0;  // == 8m for the owner of astar
+        const int xb = cen ? 0 : (((k - as) & 1) ? -xa : xa);
+        const int dstar_l = as - a0;  // == 8m for the owner of astar
         // (1) zero x_a and x_b: the Q pairs below and the C windows then read 0 there,
         //     which is exactly the fused rule's treatment of the flipped pair
         __syncwarp();
-        if (lane == 0) Xa[ah] = 0;
-        if (lane == 1) Xa[bstar >> 1] = 0;
+        if (step && sl == 0) Xa[ah] = 0;
+        if (step && sl == 1) Xa[bstar >> 1] = 0;
         __syncwarp();
         // (2) Q pairs through the flipped positions, neighbours of astar's parity:
         //     dQ(a) = -x_a* x_{2a-a*} - x_b* x_{2a-b*}, except the pair excluded from Q(a)
         //     (its upper element is L-1-a, i.e. a* = 3a - (L-1)).  The centre's Q never
         //     changes (its only pair through a* is (a*, b*), both zeroed).
-        skip = inval;
-        if (par == apar) {  // (the owner of astar has astar's parity)
-            const int ex3 = astar + L - 1;  // == 3a for the excluded pair
-            const int8_t* Xp = Xa + ((2 * a0 - astar) >> 1);
-            const int8_t* Xq = Xa + ((2 * a0 - bstar) >> 1);
+        if (step) {
+            skip = inval;
+            if (par == apar) {  // (the owner of astar has astar's parity)
+                const int ex3 = as + L - 1;  // == 3a for the excluded pair
+                const int8_t* Xp = Xa + ((2 * a0 - as) >> 1);
+                const int8_t* Xq = Xa + ((2 * a0 - bstar) >> 1);
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
-                int xp = Xp[8 * m];
-                const int xq = Xq[8 * m];
-                if (3 * (a0 + 8 * m) == ex3) xp = 0;
-                const int term = xa * xp + xb * xq;
-                if (dstar_l != 8 * m) {
-                    T[m] -= 64 * term;
-                } else {  // the pivot's own entry: its sign flips; next step's undo move
-                    xs[m] = -xs[m];
-                    skip |= 1u << m;
+                for (int m = 0; m < R; ++m) {
+                    int xp = Xp[8 * m];
+                    const int xq = Xq[8 * m];
+                    if (3 * (a0 + 8 * m) == ex3) xp = 0;
+                    const int term = xa * xp + xb * xq;
+                    if (dstar_l != 8 * m) {
+                        T[m] -= 64 * term;
+                    } else {  // the pivot's own entry: its sign flips; next step's undo move
+                        xs[m] = -xs[m];
+                        skip |= 1u << m;
+                    }
                 }
             }
         }
         // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
         int cmx = 0, esp = 0;
-        {
+        if (step) {
             const uint32_t* Xaw = apar ? w.X1w : w.X0w;
             const int awF = (P.xoff + ah + 1) >> 2;
             const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
@@ -544,7 +618,7 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
             const int mul = cen ? -2 * xa : -4 * xa;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
-                const int s = lane + 32 * jj;
+                const int s = sl + LPW * jj;
                 if (jj < nj && s < S) {
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
@@ -553,65 +627,71 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
                     for (int b = 0; b < 4; ++b) {
                         dc[b] = mul * (sbyte(fw, b) + sbyte(bw, b));
                         C[jj][b] += dc[b];
-                        cmx |= C[jj][b] + 128;  // bits above 7 set <=> |C| > 127 somewhere
                         if (P.debug_check) esp += C[jj][b] * C[jj][b];
                     }
                     w.DC[s] = pack4(dc[0], dc[1], dc[2], dc[3]);
+                    // bits above 7 of C + 128 set <=> |C| > 127 (wide kernel bytes needed)
+                    cmx |= ((C[jj][0] + 128) | (C[jj][1] + 128)) | ((C[jj][2] + 128) | (C[jj][3] + 128));
                 }
             }
         }
-        const bool wide_next = __any_sync(FULLMASK, (cmx & ~0xff) != 0);  // also syncs
+        const bool wide_next = sg.any((cmx & ~0xff) != 0);
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj) {
-            const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1);
-            const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, 31);
-            const int s = lane + 32 * jj;
-            const int cprev = s == 0 ? 0 : (lane == 0 ? wrap : up);
-            if (jj < nj && s < S) store_k_word(w, P, s, C[jj], cprev, wide_next);
+            const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1, LPW);
+            const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
+            const int s = sl + LPW * jj;
+            const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
+            if (step && jj < nj && s < S) store_k_word(w, P, s, C[jj], cprev, wide_next);
         }
-        wide = wide_next;
+        if (step) wide = wide_next;
         __syncwarp();
         // (4) write the flipped pair, C term of T, sign of the pivot's own entry, hashes
-        if (lane == 0) Xa[ah] = (int8_t)(-xa);
-        if (lane == 1 && !cen) Xa[bstar >> 1] = (int8_t)(-xb);
-        if (lane == 2) w.half[astar >> 5] ^= 1u << (astar & 31);
-        {
+        if (step) {
+            if (sl == 0) Xa[ah] = (int8_t)(-xa);
+            if (sl == 1 && !cen) Xa[bstar >> 1] = (int8_t)(-xb);
+            if (sl == 2) w.half[as >> 5] ^= 1u << (as & 31);
             const int8_t* Dm = DCb + (k - a0 - 1);  // byte t-1 of lag t = k - a
 #pragma unroll
             for (int m = 0; m < R; ++m) T[m] += sgn8 * (int)Dm[-8 * m];
         }
         if (P.debug_check) {
-            const int echk = warp_sum(esp);
-            if (echk != energy + dstar) ++diverged;
+            const int echk = sg.sum(esp);
+            if (step && echk != energy + dstar) ++diverged;
         }
-        h1 ^= fm0[astar];
-        h2 ^= fm1[astar];
-        hf ^= fmf[astar];
-        if (lane < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
-        energy += dstar;
-        best = min(best, energy);
+        if (step) {
+            h1 ^= fm0[as];
+            h2 ^= fm1[as];
+            hf ^= fmf[as];
+            if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
+            energy += dstar;
+            best = min(best, energy);
+        }
         __syncwarp();
-        if (energy < P.e_l) {
-            ++emitted;
+        const bool hit = step && energy < P.e_l;
+        if (sg.uni(hit)) {
             unsigned long long slot = 0;
-            if (lane == 0) slot = atomicAdd(P.rec_count, 1ull);
-            slot = __shfl_sync(FULLMASK, slot, 0);
-            if ((long long)slot < P.rec_cap) {
-                uint32_t* r = P.rec + slot * (unsigned long long)P.rec_words;
-                if (lane == 0) {
-                    r[0] = (uint32_t)walk;
-                    r[1] = (uint32_t)(it + 1);
-                    r[2] = (uint32_t)energy;
-                    r[3] = 0;
-                    r[4] = (uint32_t)hf;
-                    r[5] = (uint32_t)(hf >> 32);
+            if (hit && sl == 0) slot = atomicAdd(P.rec_count, 1ull);
+            slot = sg.bcast(slot);
+            if (hit) {
+                ++emitted;
+                if ((long long)slot < P.rec_cap) {
+                    uint32_t* r = P.rec + slot * (unsigned long long)P.rec_words;
+                    if (sl == 0) {
+                        r[0] = (uint32_t)walk;
+                        r[1] = (uint32_t)(it + 1);
+                        r[2] = (uint32_t)energy;
+                        r[3] = 0;
+                        r[4] = (uint32_t)hf;
+                        r[5] = (uint32_t)(hf >> 32);
+                    }
+                    for (int i = sl; i < P.hw; i += LPW) r[kRecHeader + i] = w.half[i];
                 }
-                for (int i = lane; i < P.hw; i += 32) r[kRecHeader + i] = w.half[i];
             }
         }
     }
-    if (COUNT) evals_part = warp_sum64(evals_part);
-    if (lane == 0 && P.walk_stats) {
+    if (COUNT) evals_part = sg.sum64(evals_part);
+    if (valid && sl == 0 && P.walk_stats) {
         int64_t* st = P.walk_stats + walk * kWalkStatWords;
         st[kWsIterations] = iterations;
         st[kWsEmitted] = emitted;
@@ -626,24 +706,27 @@ __device__ void run_walk_warp(const WalkParams& P, const WarpSmem& w, const uint
     __syncwarp();
 }
 
-// Resident 128-thread blocks per SM the register allocation is sized for: 4 (<= 128
-// registers) up to R = 8; wider lanes (R neighbours each) get more registers instead of
-// spilling (R = 16 needs ~200).
-template <int R>
+// Resident 128-thread blocks per SM the register allocation is sized for.  Per lane the
+// state grows with R (neighbours) and the lag words; wider lanes get more registers
+// instead of spilling.
+template <int R, int LPW>
 struct MinBlocks {
-    static constexpr int value = R <= 8 ? 4 : (R <= 12 ? 3 : 2);
+    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 3 : 2) : (R <= 12 ? 3 : 2));
 };
 
-template <int R, bool COUNT>
-__global__ void __launch_bounds__(128, MinBlocks<R>::value) saw_walk_kernel(WalkParams P, int* score_out,
-                                                                        int* corr_out) {
+template <int R, int LPW, bool COUNT>
+__global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
+    saw_walk_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
     for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
     __syncthreads();
-    const int fm_words = P.fm_words;  // u32 words, 16-byte aligned
+    constexpr int SEGS = Seg<LPW>::kSegs;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + fm_words + warp * P.warp_words;
+    const Seg<LPW> sg(lane);
+    const int seg = lane / LPW;
+    uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + P.fm_words +
+                     (warp * SEGS + seg) * P.warp_words;
     WarpSmem w;
     w.X0w = base;
     w.X1w = base + P.off_x1;
@@ -657,18 +740,20 @@ __global__ void __launch_bounds__(128, MinBlocks<R>::value) saw_walk_kernel(Walk
     w.half = base + P.off_half;
     w.bloom = base + P.off_bloom;
     const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
-    for (int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp; walk < P.nwalks;
-         walk += stride)
-        run_walk_warp<R, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, lane, score_out,
-                                corr_out);
+    for (int64_t grp = (int64_t)blockIdx.x * P.warps_per_block + warp; grp * SEGS < P.nwalks;
+         grp += stride) {
+        const int64_t walk = grp * SEGS + seg;
+        run_walk_seg<R, LPW, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, walk < P.nwalks,
+                                    sg, score_out, corr_out);
+    }
 }
 
-// Per-R launch / occupancy helpers, explicitly instantiated in saw_walk_r*.cu so that
-// the sixteen R variants compile in parallel translation units.
-template <int R>
+// Per-(R, LPW) launch / occupancy helpers, explicitly instantiated in saw_walk_r*.cu so
+// that the variants compile in parallel translation units.
+template <int R, int LPW>
 cudaError_t launch_walk_fixed(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
                               int* score_out, int* corr_out, bool count) {
-    auto kfn = count ? saw_walk_kernel<R, true> : saw_walk_kernel<R, false>;
+    auto kfn = count ? saw_walk_kernel<R, LPW, true> : saw_walk_kernel<R, LPW, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -676,12 +761,12 @@ cudaError_t launch_walk_fixed(const WalkParams& P, int grid, size_t smem, cudaSt
     return cudaGetLastError();
 }
 
-template <int R>
+template <int R, int LPW>
 int blocks_per_sm_fixed(const WalkParams& P, size_t smem) {
     int n = 0;
-    cudaFuncSetAttribute(saw_walk_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, saw_walk_kernel<R, false>,
+    cudaFuncSetAttribute(saw_walk_kernel<R, LPW, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, saw_walk_kernel<R, LPW, false>,
                                                       P.warps_per_block * 32, smem) != cudaSuccess)
         return 0;
     return n;

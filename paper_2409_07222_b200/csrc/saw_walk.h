@@ -7,9 +7,9 @@
 #include "saw_device.h"
 
 namespace labs_b200 {
-template <int R>
+template <int R, int LPW>
 cudaError_t launch_walk_fixed(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
                               int* score_out, int* corr_out, bool count);
-template <int R>
+template <int R, int LPW>
 int blocks_per_sm_fixed(const WalkParams& P, size_t smem);
 }  // namespace labs_b200

@@ -1,17 +1,29 @@
-// saw_walk_r1_4.cu -- explicit instantiations of K1 for R = 1..4 (parallel build).
+// saw_walk_r1_4.cu -- explicit instantiations of K1 (LPW = 32 and 16) for R = 1..4 (parallel build).
 #include "saw_walk.cuh"
 
 namespace labs_b200 {
-template cudaError_t launch_walk_fixed<1>(const WalkParams&, int, size_t, cudaStream_t, int*,
-                                           int*, bool);
-template int blocks_per_sm_fixed<1>(const WalkParams&, size_t);
-template cudaError_t launch_walk_fixed<2>(const WalkParams&, int, size_t, cudaStream_t, int*,
-                                           int*, bool);
-template int blocks_per_sm_fixed<2>(const WalkParams&, size_t);
-template cudaError_t launch_walk_fixed<3>(const WalkParams&, int, size_t, cudaStream_t, int*,
-                                           int*, bool);
-template int blocks_per_sm_fixed<3>(const WalkParams&, size_t);
-template cudaError_t launch_walk_fixed<4>(const WalkParams&, int, size_t, cudaStream_t, int*,
-                                           int*, bool);
-template int blocks_per_sm_fixed<4>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<1, 32>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<1, 32>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<1, 16>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<1, 16>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<2, 32>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<2, 32>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<2, 16>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<2, 16>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<3, 32>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<3, 32>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<3, 16>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<3, 16>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<4, 32>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<4, 32>(const WalkParams&, size_t);
+template cudaError_t launch_walk_fixed<4, 16>(const WalkParams&, int, size_t, cudaStream_t,
+                                               int*, int*, bool);
+template int blocks_per_sm_fixed<4, 16>(const WalkParams&, size_t);
 }  // namespace labs_b200
