@@ -1,15 +1,13 @@
 // saw_walk.cuh -- K1, the sm_100a walk kernel of Step 1 of the dual-step LABS search
-// (templates; instantiated per R in saw_walk_r*.cu, launched from saw_kernels.cu).
+// (templates; instantiated per (R, LPW) in saw_walk_r*.cu, launched from saw_kernels.cu).
 //
-// K1 saw_walk_kernel : one warp = one self-avoiding walk (run_walk, saw.cpp:117-149).
+// K1 saw_walk_kernel : 32 or 16 lanes = one self-avoiding walk (run_walk, saw.cpp:117-149).
 //                      Fuses the Bloom probe, the skew flip-delta of every free
 //                      neighbour (skew_flip_delta_fast, skew.cpp:60-93), the
 //                      lexicographic argmin (best_neighbour, saw.cpp:106-115), the
 //                      apply (apply_skew_flip, skew.cpp:95-105), the Bloom insert
 //                      and the E < E_l sieve with compaction into a device
 //                      record buffer (sink.emit, saw.cpp:143-146).
-// K3 saw_seed_kernel : xoshiro256** streams -> initial halves
-//                      (Rng + init_partitioned_sequence, rng.hpp:21-45, saw.cpp:65-75).
 //
 // Arithmetic.  For a skew-symmetric pivot the four sign products of
 // the reference's fused delta pair up (x_b x_{b+-kk} = x_a x_{a-+kk}), so for half
@@ -22,8 +20,9 @@
 // the symmetric kernel K[d] = C_{2|d|}: G(a) = sum_i X_par[i] K[i - a/2].  A lane owns
 // neighbours a0, a0+8, ..., so one X word is shared by its R neighbours and the kernel
 // window slides by one word per neighbour: 4 positions per IDP4A (int8 C), plus a
-// second IDP4A on the high bytes while some |C| > 127.  16N+32Q is kept per neighbour
-// in shared memory and updated in O(1) per flip.  Everything is exact integer math.
+// second IDP4A on the high bytes while some |C| > 127.  The rest of the delta,
+// T(a) = 16N + 32Q + 8(-1)^(k-a) C_{2(k-a)}, is kept per neighbour in the owning lane's
+// registers and updated in O(1) per flip.  Everything is exact integer math.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -147,10 +146,6 @@ struct WarpSmem {
     uint32_t* half;   // half bits
     uint32_t* bloom;  // visited filter
 };
-
-__device__ __forceinline__ int xval(const WarpSmem& w, const WalkParams& P, int j) {
-    return (j & 1) ? w.X1[P.xoff + (j >> 1)] : w.X0[P.xoff + (j >> 1)];
-}
 
 // Sign of full-sequence position j of the skew expansion of `half` (skew.cpp:14-26).
 __device__ __forceinline__ int x_of_half(const uint32_t* half, int k, int j) {
