@@ -13,10 +13,9 @@
 // sequence lives in shared memory as two parity byte arrays.  A step's energy change
 //     dE = sum_t dc_t (2 C_{2t} + dc_t),   dc_t = mul * (x_{a+2t} + x_{a-2t} - [t = k-a] x_b)
 // (mul = -4 x_a, or -2 x_a for the centre; the same fused even-lag rule as the walk
-// kernel's apply) is accumulated per lane for 32 steps in registers and then reduced
-// with one 31-shuffle transpose-reduction + a lane scan, so each lane ends up holding
-// the energy of one configuration: the warp-wide reduction costs ~4 instructions per
-// step instead of 10.  Exact integer arithmetic throughout.
+// kernel's apply) is reduced per step with one REDUX (its result is consumed only after
+// 32 steps, off the critical path), lane s keeping step s's total; a lane scan then gives
+// every lane the energy of one configuration.  Exact integer arithmetic throughout.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -49,12 +48,10 @@ struct EnumLaunch {
     int64_t* chunk_best;                // [nchunks][2]: best E, its first g
 };
 
-__device__ __forceinline__ uint32_t sel4(int o) {
-    return (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
-}
-__device__ __forceinline__ uint32_t sel4r(int o) {
-    return (uint32_t)((o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
-}
+// PRMT selector of bytes o..o+3 of a word pair: o | (o+1)<<4 | (o+2)<<8 | (o+3)<<12
+__device__ __forceinline__ uint32_t sel4(int o) { return 0x3210u + 0x1111u * (uint32_t)o; }
+// bytes o+3..o (reversed): (o+3) | (o+2)<<4 | (o+1)<<8 | o<<12
+__device__ __forceinline__ uint32_t sel4r(int o) { return 0x0123u + 0x1111u * (uint32_t)o; }
 __device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
 
 template <int NJ>
@@ -133,64 +130,56 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     }
 
     // ---- Gray steps g = g0+1 .. g1-1 in batches of 32 ----
+    // ctz(g0 + i) = ctz(i) when the chunk start is a multiple of 2^chunk_log2 (every chunk
+    // when g_begin is aligned); else the 64-bit path.
+    const bool aligned = (g0 & ((1ull << P.chunk_log2) - 1)) == 0;
     const uint64_t nsteps = g1 - g0 - 1;
     for (uint64_t s0 = 0; s0 < nsteps; s0 += 32) {
-        int part[32];
+        const int nb = (int)(nsteps - s0 < 32 ? nsteps - s0 : 32);
+        int mine = 0;  // dE of step s0 + lane (REDUX result of step `lane`)
+        for (int s = 0; s < nb; ++s) {  // (rolled: small code, no instruction-cache misses)
+            const uint64_t i = s0 + s + 1;
+            const int tz = aligned ? __ffs((unsigned)i) - 1 : __ffsll((long long)(g0 + i)) - 1;
+            const int a = P.p + tz;
+            const int ah = a >> 1;
+            int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
+            const uint32_t* Xaw = (a & 1) ? X1w : X0w;
+            const int xa = Xa[ah];
+            const bool cen = a == k;
+            const int tstar = cen ? -3 : k - a;  // (-3: matches no lag word)
+            const int xb = ((k - a) & 1) ? -xa : xa;
+            const int mul = cen ? -2 * xa : -4 * xa;
+            const int awF = (P.xoff + ah + 1) >> 2;
+            const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
+            const int awB = (P.xoff + ah - 4) >> 2;
+            const uint32_t asB = sel4r((P.xoff + ah) & 3);
+            const int tw = (tstar - 1) >> 2;
+            const uint32_t tmask = ~(0xffu << (8 * ((tstar - 1) & 3)));
+            int acc = 0;
 #pragma unroll
-        for (int s = 0; s < 32; ++s) {
-            part[s] = 0;
-            if (s0 + s < nsteps) {  // warp-uniform
-                const uint64_t g = g0 + 1 + s0 + s;
-                const int a = P.p + (__ffsll((long long)g) - 1);
-                const int ah = a >> 1;
-                int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
-                const uint32_t* Xaw = (a & 1) ? X1w : X0w;
-                const int xa = Xa[ah];
-                const bool cen = a == k;
-                const int tstar = cen ? -1 : k - a;
-                const int xb = ((k - a) & 1) ? -xa : xa;
-                const int mul = cen ? -2 * xa : -4 * xa;
-                const int awF = (P.xoff + ah + 1) >> 2;
-                const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
-                const int awB = (P.xoff + ah - 4) >> 2;
-                const uint32_t asB = sel4r((P.xoff + ah) & 3);
-                int acc = 0;
+            for (int j = 0; j < NJ; ++j) {
+                const int sw = lane + 32 * j;
+                if (sw < P.S) {  // lanes past the lag range read nothing
+                    uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
+                    const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
+                    // the fused rule's [t = k-a] x_b term: the forward byte at t* is x_b
+                    if (sw == tw) fw &= tmask;
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const int sw = lane + 32 * j;
-                    if (sw < P.S) {  // lanes past the lag range read nothing
-                        const uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
-                        const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            const int t = 4 * sw + 1 + b;
-                            int v = sbyte(fw, b) + sbyte(bw, b);
-                            if (t == tstar) v -= xb;
-                            const int dc = mul * v;  // 0 for t > k (zero padding)
-                            acc += dc * (2 * C[j][b] + dc);
-                            C[j][b] += dc;
-                        }
+                    for (int b = 0; b < 4; ++b) {
+                        const int dc = mul * (sbyte(fw, b) + sbyte(bw, b));  // 0 beyond k
+                        acc += dc * (2 * C[j][b] + dc);
+                        C[j][b] += dc;
                     }
                 }
-                part[s] = acc;
-                __syncwarp();
-                if (lane == 0) Xa[ah] = (int8_t)(-xa);
-                if (lane == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
-                __syncwarp();
             }
+            const int tot = __reduce_add_sync(FULLMASK, acc);
+            if (lane == s) mine = tot;
+            __syncwarp();
+            if (lane == 0) Xa[ah] = (int8_t)(-xa);
+            if (lane == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
+            __syncwarp();
         }
-        // transpose-reduce: lane l ends with sum over lanes of part[l]
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-            const bool up = lane & off;
-#pragma unroll
-            for (int i = 0; i < off; ++i) {
-                const int send = up ? part[i] : part[i + off];
-                const int keep = up ? part[i + off] : part[i];
-                part[i] = keep + __shfl_xor_sync(FULLMASK, send, off);
-            }
-        }
-        int e = part[0];  // dE of step s0 + lane
+        int e = mine;  // dE of step s0 + lane
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(FULLMASK, e, o);

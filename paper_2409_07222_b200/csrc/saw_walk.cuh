@@ -65,12 +65,10 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t sel4(int o) {  // bytes o..o+3 of a word pair
-    return (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
-}
-__device__ __forceinline__ uint32_t sel4r(int o) {  // bytes o+3..o (reversed)
-    return (uint32_t)((o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
-}
+// PRMT selector of bytes o..o+3 of a word pair: o | (o+1)<<4 | (o+2)<<8 | (o+3)<<12
+__device__ __forceinline__ uint32_t sel4(int o) { return 0x3210u + 0x1111u * (uint32_t)o; }
+// bytes o+3..o (reversed): (o+3) | (o+2)<<4 | (o+1)<<8 | o<<12
+__device__ __forceinline__ uint32_t sel4r(int o) { return 0x0123u + 0x1111u * (uint32_t)o; }
 // sign-extended byte b of w
 __device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
 
