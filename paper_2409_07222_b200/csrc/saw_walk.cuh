@@ -101,6 +101,28 @@ __device__ __forceinline__ void g_step(const uint32_t* __restrict__ Xw,
     }
 }
 
+template <int R, bool WIDE, int J>
+struct GTail {
+    static __device__ __forceinline__ void run(const uint32_t* __restrict__ Xw,
+                                               const uint32_t* __restrict__ Kl,
+                                               const uint32_t* __restrict__ Kh, int w0, int rem,
+                                               int kb, uint32_t sel, uint32_t (&KL)[R],
+                                               uint32_t (&KH)[R], uint32_t& rl, uint32_t& rh,
+                                               int (&acc)[R], int (&acch)[R]) {
+        if (J < rem) {
+            g_step<R, WIDE>(Xw, Kl, Kh, w0 + J, J, kb, sel, KL, KH, rl, rh, acc, acch);
+            GTail<R, WIDE, J + 1>::run(Xw, Kl, Kh, w0, rem, kb, sel, KL, KH, rl, rh, acc, acch);
+        }
+    }
+};
+template <int R, bool WIDE>
+struct GTail<R, WIDE, R> {
+    static __device__ __forceinline__ void run(const uint32_t* __restrict__, const uint32_t* __restrict__,
+                                               const uint32_t* __restrict__, int, int, int,
+                                               uint32_t, uint32_t (&)[R], uint32_t (&)[R],
+                                               uint32_t&, uint32_t&, int (&)[R], int (&)[R]) {}
+};
+
 template <int R, bool WIDE>
 __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
                                              const uint32_t* __restrict__ Kl,
@@ -122,12 +144,9 @@ __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
         for (int j = 0; j < R; ++j)
             g_step<R, WIDE>(Xw, Kl, Kh, w0 + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
     }
-    if (nfull < nwx) {
-#pragma unroll
-        for (int j = 0; j < R; ++j)
-            if (nfull + j < nwx)
-                g_step<R, WIDE>(Xw, Kl, Kh, nfull + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
-    }
+    // remainder steps j = 0 .. nwx - nfull - 1: nested guards, so a remainder of r costs
+    // r + 1 tests instead of R
+    GTail<R, WIDE, 0>::run(Xw, Kl, Kh, nfull, nwx - nfull, kb, sel, KL, KH, rl, rh, acc, acch);
 }
 
 // ---------------------------------------------------------------------------
