@@ -441,8 +441,9 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     const bool one_key = L <= 1001;
     bool active = valid;  // this segment's walk is still running
 
-    for (long long it = 0;; ++it) {
-        const bool cont = active && it < t_i;
+    const int t_i32 = (int)t_i;  // T_i < 2^28 (make_walk_params: Bloom bits < 2^32)
+    for (int it = 0;; ++it) {
+        const bool cont = active && it < t_i32;
         if (!sg.uni(cont)) break;
         // ---- G for all owned neighbours (the O(L) part: IDP4A sliding dot product) ----
         int acc[R], acch[R];
@@ -456,7 +457,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         int delta[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) {
-            const int gg = wide ? acc[m] + 256 * acch[m] : acc[m];
+            // (acch = 0 from the narrow G loop; a non-wide segment in a wide warp ignores it)
+            const int gg = acc[m] + (wide ? 256 * acch[m] : 0);
             delta[m] = T[m] - xs[m] * gg;
         }
         if (score_out) {
@@ -610,12 +612,10 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                     const int xq = Xq[8 * m];
                     if (3 * (a0 + 8 * m) == ex3) xp = 0;
                     const int term = xa * xp + xb * xq;
-                    if (dstar_l != 8 * m) {
-                        T[m] -= 64 * term;
-                    } else {  // the pivot's own entry: its sign flips; next step's undo move
-                        xs[m] = -xs[m];
-                        skip |= 1u << m;
-                    }
+                    const bool own = dstar_l == 8 * m;  // the pivot's own entry (undo move)
+                    T[m] -= own ? 0 : 64 * term;
+                    xs[m] = own ? -xs[m] : xs[m];
+                    skip |= own ? (1u << m) : 0u;
                 }
             }
         }
