@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <chrono>
 #include <cstdio>
@@ -366,10 +367,15 @@ struct SinkChain {
     bool stop = false;
     bool aborted = false;
     std::vector<int8_t> half, full;
-    // pending batch
+    // pending batch: accepted records (half bits still packed), expanded at flush
+    std::vector<const uint32_t*> b_half;
     std::vector<int8_t> b_signs;
     std::vector<int64_t> b_energy, b_walker, b_restart, b_iter;
     std::vector<int32_t> b_class;
+    // full position j of the skew expansion (skew.cpp:14-26) reads half bit src[j], negated
+    // when neg[j]
+    std::vector<int16_t> x_src;
+    std::vector<uint8_t> x_neg;
 
     void deliver(uint32_t walker, int64_t restart, const WalkRecordView& r) {
         if (!seen.insert(r.hash).second) return;
@@ -385,11 +391,7 @@ struct SinkChain {
         if (aborted) return;
         const int cls = static_cast<int>(walker % static_cast<uint32_t>(d->nprefix));
         if (emit_batch) {
-            const size_t off = b_signs.size();
-            b_signs.resize(off + static_cast<size_t>(d->L));
-            half.resize(static_cast<size_t>(d->kp1));
-            half_bits_to_signs(r.half, d->kp1, half.data());
-            expand_skew(half.data(), d->kp1, b_signs.data() + off);
+            b_half.push_back(r.half);
             b_energy.push_back(r.energy);
             b_walker.push_back(walker);
             b_restart.push_back(restart);
@@ -417,11 +419,56 @@ struct SinkChain {
         }
     }
 
+    void expand_range(size_t i0, size_t i1) {
+        const int L = d->L;
+        for (size_t i = i0; i < i1; ++i) {
+            const uint32_t* bits = b_half[i];
+            int8_t* out = b_signs.data() + i * static_cast<size_t>(L);
+            for (int j = 0; j < L; ++j) {
+                const int src = x_src[static_cast<size_t>(j)];
+                const int bit = static_cast<int>((bits[src >> 5] >> (src & 31)) & 1u) ^ x_neg[static_cast<size_t>(j)];
+                out[j] = bit ? 1 : -1;
+            }
+        }
+    }
+
+    // Expands the pending records (in parallel for large batches; the order and the
+    // dedup decisions were fixed in deliver) and hands them to emit_batch.  Must run
+    // before the records' batch buffer is released.
     void flush() {
-        if (!emit_batch || b_energy.empty() || aborted) return;
+        if (!emit_batch || b_energy.empty() || aborted) {
+            b_half.clear();
+            b_energy.clear(), b_walker.clear(), b_restart.clear(), b_iter.clear(), b_class.clear();
+            return;
+        }
+        const int L = d->L, k = d->k;
+        if (static_cast<int>(x_src.size()) != L) {
+            x_src.resize(static_cast<size_t>(L));
+            x_neg.resize(static_cast<size_t>(L));
+            for (int j = 0; j < L; ++j) {
+                const int i = j > k ? j - k : 0;
+                x_src[static_cast<size_t>(j)] = static_cast<int16_t>(j > k ? k - i : j);
+                x_neg[static_cast<size_t>(j)] = static_cast<uint8_t>(i & 1);
+            }
+        }
+        const size_t n = b_energy.size();
+        b_signs.resize(n * static_cast<size_t>(L));
+        const size_t nthreads = std::min<size_t>(
+            n / 1024, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+        if (nthreads <= 1) {
+            expand_range(0, n);
+        } else {
+            std::vector<std::thread> th;
+            const size_t chunk = (n + nthreads - 1) / nthreads;
+            for (size_t t = 0; t < nthreads; ++t)
+                th.emplace_back([this, t, chunk, n] {
+                    expand_range(t * chunk, std::min(n, (t + 1) * chunk));
+                });
+            for (auto& x : th) x.join();
+        }
         labs_candidate_batch b{};
-        b.count = static_cast<int32_t>(b_energy.size());
-        b.length = d->L;
+        b.count = static_cast<int32_t>(n);
+        b.length = L;
         b.prefix_len = d->p;
         b.origin = 0;
         b.signs = b_signs.data();
@@ -432,12 +479,8 @@ struct SinkChain {
         b.prefix_class = b_class.data();
         b.prefixes = d->p > 0 ? d->prefixes.data() : nullptr;
         if (emit_batch(user, &b) != 0) aborted = true;
-        b_signs.clear();
-        b_energy.clear();
-        b_walker.clear();
-        b_restart.clear();
-        b_iter.clear();
-        b_class.clear();
+        b_half.clear();
+        b_energy.clear(), b_walker.clear(), b_restart.clear(), b_iter.clear(), b_class.clear();
     }
 };
 
@@ -539,6 +582,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                 }
                 if (acc.diverged) break;
             }
+            sink.flush();  // the batch's record buffer dies with `b`
             (void)segs;
         };
 
@@ -595,10 +639,18 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                             }
                             nw += segs[i].r1 - segs[i].r0;
                         }
+                        const auto tA = std::chrono::steady_clock::now();
                         dr.seed(segs, d, cfg.seed, states, init, nw, b);
                         carry_w = segs.back().walker;
                         carry_state = states.back();
+                        const auto tB = std::chrono::steady_clock::now();
                         dr.walk(nw, b);
+                        const auto tC = std::chrono::steady_clock::now();
+                        if (std::getenv("LABS_TIMING"))
+                            std::fprintf(stderr, "[labs] seed %.2f ms, walk+d2h %.2f ms (kernel %.2f)\n",
+                                         std::chrono::duration<double, std::milli>(tB - tA).count(),
+                                         std::chrono::duration<double, std::milli>(tC - tB).count(),
+                                         b.kernel_ms);
                         outs[static_cast<size_t>(g)].push_back(std::move(b));
                         segs_all[static_cast<size_t>(g)].push_back(segs);
                     }
@@ -627,7 +679,13 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                 acc.st.seed_ms = std::max(acc.st.seed_ms, sms);
             }
             if (ngpu == 1) {
+                const auto tD = std::chrono::steady_clock::now();
                 for (size_t bi = 0; bi < outs[0].size(); ++bi) process_batch(segs_all[0][bi], outs[0][bi]);
+                if (std::getenv("LABS_TIMING"))
+                    std::fprintf(stderr, "[labs] host replay %.2f ms, prep %.2f ms\n",
+                                 std::chrono::duration<double, std::milli>(
+                                     std::chrono::steady_clock::now() - tD).count(),
+                                 std::chrono::duration<double, std::milli>(tD - t0).count());
             } else {
                 // merge: walks of all devices in (walker, restart) order
                 struct Ref {
@@ -669,6 +727,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                         acc.best_set = true;
                     }
                 }
+                sink.flush();  // before the devices' record buffers are released
             }
         } else {
             // Coupled stop conditions: ordered batches, stop replay exactly like --threads 1.
