@@ -118,9 +118,11 @@ def ncu_traffic(walks):
 
 
 def cpu_sample(walkers_hint=None):
-    """Size of the bounded CPU sample: walkers [0, n) x 1 restart of the C4 workload."""
+    """Size of the bounded CPU sample: walkers [0, n) x 1 restart of the C4 workload
+    (BENCH_CPU_WALKERS overrides n; the CPU tests use a tiny sample)."""
     cores = os.cpu_count() or 1
-    n = walkers_hint or min(WALKERS_PER_GPU, max(16, CPU_WALKS_PER_CORE * cores))
+    n = walkers_hint or int(os.environ.get("BENCH_CPU_WALKERS", "0")) or \
+        min(WALKERS_PER_GPU, max(16, CPU_WALKS_PER_CORE * cores))
     return cores, n
 
 
