@@ -67,6 +67,27 @@ struct DevBuf {
     }
 };
 
+// Grow-only pinned host staging (async D2H drains of the record buffer and walk stats).
+template <typename T>
+struct PinnedBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void reserve(size_t count) {
+        if (count <= n) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        LABS_CUDA(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        n = count;
+    }
+};
+
 // One restart range of one walker, in --threads 1 order.
 struct Segment {
     uint32_t walker;
@@ -103,6 +124,9 @@ public:
     DevBuf<int64_t> stats, seg_rest, seg_off;
     DevBuf<int32_t> seg_init;
     DevBuf<unsigned long long> rec_count;
+    PinnedBuf<uint32_t> h_rec;
+    PinnedBuf<int64_t> h_stats;
+    PinnedBuf<unsigned long long> h_count;
     int64_t rec_cap = 0;
 
     ~DeviceRunner() {
@@ -245,9 +269,16 @@ public:
             LABS_CUDA(cudaEventRecord(ev[0], st));
             LABS_CUDA(launch_saw_walk(P, grid, st, score_out, corr_out));
             LABS_CUDA(cudaEventRecord(ev[1], st));
-            unsigned long long cnt = 0;
-            LABS_CUDA(cudaMemcpyAsync(&cnt, rec_count.p, sizeof cnt, cudaMemcpyDeviceToHost, st));
+            h_count.reserve(1);
+            LABS_CUDA(cudaMemcpyAsync(h_count.p, rec_count.p, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, st));
+            // the per-walk stats do not depend on the record count: drain them meanwhile
+            h_stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
+            LABS_CUDA(cudaMemcpyAsync(h_stats.p, stats.p,
+                                      static_cast<size_t>(nwalks) * kWalkStatWords * 8,
+                                      cudaMemcpyDeviceToHost, st));
             LABS_CUDA(cudaStreamSynchronize(st));
+            const unsigned long long cnt = *h_count.p;
             float ms = 0;
             LABS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
             out.kernel_ms += ms;
@@ -259,12 +290,14 @@ public:
             out.nrec = static_cast<int64_t>(cnt);
             out.rec.resize(static_cast<size_t>(cnt) * wp.rec_words);
             out.stats.resize(static_cast<size_t>(nwalks) * kWalkStatWords);
-            if (cnt)
-                LABS_CUDA(cudaMemcpyAsync(out.rec.data(), rec.p, out.rec.size() * 4,
+            if (cnt) {
+                h_rec.reserve(out.rec.size());
+                LABS_CUDA(cudaMemcpyAsync(h_rec.p, rec.p, out.rec.size() * 4,
                                           cudaMemcpyDeviceToHost, st));
-            LABS_CUDA(cudaMemcpyAsync(out.stats.data(), stats.p, out.stats.size() * 8,
-                                      cudaMemcpyDeviceToHost, st));
-            LABS_CUDA(cudaStreamSynchronize(st));
+                LABS_CUDA(cudaStreamSynchronize(st));
+                std::memcpy(out.rec.data(), h_rec.p, out.rec.size() * 4);
+            }
+            std::memcpy(out.stats.data(), h_stats.p, out.stats.size() * 8);
             out.d2h += static_cast<int64_t>(sizeof cnt + out.rec.size() * 4 + out.stats.size() * 8);
             return;
         }
