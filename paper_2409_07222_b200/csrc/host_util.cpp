@@ -218,7 +218,7 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.off_c16 = wp.off_kh + wp.kwords;
     wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
     wp.off_dc = wp.off_kq + round_up(wp.kp1, 4);
-    wp.off_half = wp.off_dc + round_up(wp.S + 1, 4);
+    wp.off_half = wp.off_dc;  // (no per-lag dc array: T's C term reads the sequence)
     wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
     wp.warp_words = wp.off_bloom + wp.bloom_words;
     const int fm_words = round_up(3 * wp.kp1 * 2, 4);

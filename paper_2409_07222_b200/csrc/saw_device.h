@@ -17,7 +17,6 @@ constexpr int kRecHeader = 6;      // record header: walk, iteration, energy, fl
 //            (KH only maintained while some |C| > 127)
 //   C16    : int16 C_{2t}, t = 1..4S (pairs per word)
 //   KQ     : int32 per half index a: 16 N(a) + 32 Q(a)  (a < k),  4 N + 8 Q (a = k)
-//   DC     : word 0 = 0, then the last step's dc per lag (byte t-1 of words 1.. = lag t)
 //   HALF   : packed current half,  BLOOM : visited filter bits
 struct WalkParams {
     int32_t L, k, kp1, p;          // L = 2k+1, half length k+1, prefix length p

@@ -25,6 +25,9 @@
 // registers and updated in O(1) per flip.  Everything is exact integer math.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef LABS_PHASE_CLOCKS
+#include <cstdio>
+#endif
 
 #include "saw_device.h"
 #include "saw_walk.h"
@@ -159,7 +162,6 @@ struct WarpSmem {
     uint32_t* KH;     // kernel high bytes
     uint32_t* C16;    // int16 C_{2t}, t = 4s+1..4s+4 in words 2s, 2s+1
     int* KQ;          // 16N+32Q per half index (walk initialisation only)
-    uint32_t* DC;     // dc of the last step per lag, byte t-1 = lag t; DC[-1] = 0
     uint32_t* half;   // half bits
     uint32_t* bloom;  // visited filter
 };
@@ -325,7 +327,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         (par ? w.X1w : w.X0w)[word] = v;
     }
     for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
-    if (sl == 0) w.DC[-1] = 0;  // dc of "lag 0" (the centre neighbour has no C term)
     {
         uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
         for (int i = sl; i < (P.bloom_words >> 2); i += LPW) b4[i] = make_uint4(0, 0, 0, 0);
@@ -403,7 +404,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             }
         }
     }
-    const int8_t* DCb = reinterpret_cast<const int8_t*>(w.DC);  // byte t-1 = dc of lag t
 
     // ---- half hashes h1, h2 (saw.cpp:77-89) and the initial Bloom insert ----
     uint64_t h1 = 0, h2 = 0;
@@ -442,6 +442,12 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     bool active = valid;  // this segment's walk is still running
 
     const int t_i32 = (int)t_i;  // T_i < 2^28 (make_walk_params: Bloom bits < 2^32)
+#ifdef LABS_PHASE_CLOCKS
+    long long ph_g = 0, ph_arg = 0, ph_apply = 0, ph_t = clock64();
+#define LABS_PHASE(acc) { const long long _t = clock64(); acc += _t - ph_t; ph_t = _t; }
+#else
+#define LABS_PHASE(acc)
+#endif
     for (int it = 0;; ++it) {
         const bool cont = active && it < t_i32;
         if (!sg.uni(cont)) break;
@@ -469,6 +475,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             break;
         }
 
+        LABS_PHASE(ph_g)
         // ---- choose: lowest (delta, hp) among unvisited (best_neighbour, saw.cpp:106-115) ----
         if (COUNT && cont) {
 #pragma unroll
@@ -580,6 +587,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         }
         const bool step = cont && astar >= 0;  // segment-uniform
 
+        LABS_PHASE(ph_arg)
         // ---- apply the skew flip at astar (apply_skew_flip, skew.cpp:95-105) ----
         if (step) ++iterations;
         const int as = step ? astar : P.p;  // addresses stay in range for idle segments
@@ -596,12 +604,22 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         if (step && sl == 0) Xa[ah] = 0;
         if (step && sl == 1) Xa[bstar >> 1] = 0;
         __syncwarp();
-        // (2) Q pairs through the flipped positions, neighbours of astar's parity:
+        // (2) T updates, all from the (zeroed) pre-step sequence, so their loads issue together
+        //     with the C update's:
+        //   C term: T(a) += 8 (-1)^(k-a) dc_{k-a}, dc_t = mul (x_{a*+2t} + x_{a*-2t}); the zeroed
+        //     x_a*, x_b* make t = 0 (the centre) and t = k-a* (the fused rule) come out right.
+        //   Q pairs through the flipped positions, neighbours of astar's parity:
         //     dQ(a) = -x_a* x_{2a-a*} - x_b* x_{2a-b*}, except the pair excluded from Q(a)
         //     (its upper element is L-1-a, i.e. a* = 3a - (L-1)).  The centre's Q never
         //     changes (its only pair through a* is (a*, b*), both zeroed).
+        const int mul = cen ? -2 * xa : -4 * xa;
         if (step) {
             skip = inval;
+            const int8_t* Xf = Xa + ah + (k - a0);  // x_{a*+2t}, t = k - a = (k - a0) - 8m
+            const int8_t* Xg = Xa + ah - (k - a0);  // x_{a*-2t}
+            const int cmul = sgn8 * mul;
+#pragma unroll
+            for (int m = 0; m < R; ++m) T[m] += cmul * ((int)Xf[-8 * m] + (int)Xg[8 * m]);
             if (par == apar) {  // (the owner of astar has astar's parity)
                 const int ex3 = as + L - 1;  // == 3a for the excluded pair
                 const int8_t* Xp = Xa + ((2 * a0 - as) >> 1);
@@ -627,7 +645,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
             const int awB = (P.xoff + ah - 4) >> 2;
             const uint32_t asB = sel4r((P.xoff + ah) & 3);
-            const int mul = cen ? -2 * xa : -4 * xa;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
@@ -641,7 +658,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                         C[jj][b] += dc[b];
                         if (P.debug_check) esp += C[jj][b] * C[jj][b];
                     }
-                    w.DC[s] = pack4(dc[0], dc[1], dc[2], dc[3]);
                     // bits above 7 of C + 128 set <=> |C| > 127 (wide kernel bytes needed)
                     cmx |= ((C[jj][0] + 128) | (C[jj][1] + 128)) | ((C[jj][2] + 128) | (C[jj][3] + 128));
                 }
@@ -658,14 +674,11 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         }
         if (step) wide = wide_next;
         __syncwarp();
-        // (4) write the flipped pair, C term of T, sign of the pivot's own entry, hashes
+        // (4) write the flipped pair, hashes, Bloom insert
         if (step) {
             if (sl == 0) Xa[ah] = (int8_t)(-xa);
             if (sl == 1 && !cen) Xa[bstar >> 1] = (int8_t)(-xb);
             if (sl == 2) w.half[as >> 5] ^= 1u << (as & 31);
-            const int8_t* Dm = DCb + (k - a0 - 1);  // byte t-1 of lag t = k - a
-#pragma unroll
-            for (int m = 0; m < R; ++m) T[m] += sgn8 * (int)Dm[-8 * m];
         }
         if (P.debug_check) {
             const int echk = sg.sum(esp);
@@ -680,6 +693,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             best = min(best, energy);
         }
         __syncwarp();
+        LABS_PHASE(ph_apply)
         const bool hit = step && energy < P.e_l;
         if (sg.uni(hit)) {
             unsigned long long slot = 0;
@@ -702,6 +716,13 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             }
         }
     }
+#ifdef LABS_PHASE_CLOCKS
+    if (walk < 4 && sl == 0 && valid)
+        printf("[phase] walk %lld iters %lld  G %.0f  argmin+probe %.0f  apply %.0f cycles/iter\n",
+               (long long)walk, iterations, (double)ph_g / iterations, (double)ph_arg / iterations,
+               (double)ph_apply / iterations);
+#endif
+#undef LABS_PHASE
     if (COUNT) evals_part = sg.sum64(evals_part);
     if (valid && sl == 0 && P.walk_stats) {
         int64_t* st = P.walk_stats + walk * kWalkStatWords;
@@ -748,7 +769,6 @@ __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
     w.KH = base + P.off_kh;
     w.C16 = base + P.off_c16;
     w.KQ = reinterpret_cast<int*>(base + P.off_kq);
-    w.DC = base + P.off_dc + 1;
     w.half = base + P.off_half;
     w.bloom = base + P.off_bloom;
     const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
