@@ -598,6 +598,16 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         const int xa = Xa[ah];
         const int xb = cen ? 0 : (((k - as) & 1) ? -xa : xa);
         const int dstar_l = as - a0;  // == 8m for the owner of astar
+        // hashes of the new pivot and its Bloom insert depend on nothing below: issue them
+        // first so they overlap the apply (the insert reuses the accepted probe's index)
+        if (step) {
+            h1 ^= fm0[as];
+            h2 ^= fm1[as];
+            hf ^= fmf[as];
+            if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
+            energy += dstar;
+            best = min(best, energy);
+        }
         // (1) zero x_a and x_b: the Q pairs below and the C windows then read 0 there,
         //     which is exactly the fused rule's treatment of the flipped pair
         __syncwarp();
@@ -682,15 +692,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         }
         if (P.debug_check) {
             const int echk = sg.sum(esp);
-            if (step && echk != energy + dstar) ++diverged;
-        }
-        if (step) {
-            h1 ^= fm0[as];
-            h2 ^= fm1[as];
-            hf ^= fmf[as];
-            if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
-            energy += dstar;
-            best = min(best, energy);
+            if (step && echk != energy) ++diverged;  // (energy already includes dstar)
         }
         __syncwarp();
         LABS_PHASE(ph_apply)
