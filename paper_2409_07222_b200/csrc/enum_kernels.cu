@@ -52,7 +52,13 @@ struct EnumLaunch {
 __device__ __forceinline__ uint32_t sel4(int o) { return 0x3210u + 0x1111u * (uint32_t)o; }
 // bytes o+3..o (reversed): (o+3) | (o+2)<<4 | (o+1)<<8 | o<<12
 __device__ __forceinline__ uint32_t sel4r(int o) { return 0x0123u + 0x1111u * (uint32_t)o; }
-__device__ __forceinline__ int sbyte(uint32_t w, int b) { return (int)(int8_t)(w >> (8 * b)); }
+__device__ __forceinline__ int sbyte(uint32_t w, int b) {  // one PRMT, sign-replicate mode
+    // (selector nibble 8|b copies the sign of byte b; __byte_perm drops that bit, so PTX)
+    uint32_t r;
+    const uint32_t sel = (uint32_t)(b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+    return (int)r;
+}
 
 template <int NJ>
 __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t chunk, int lane) {
