@@ -135,9 +135,21 @@ int cmd_enumerate(int argc, char** argv) {
         const double f = to_d(v["--target-f"], "--target-f");
         el = static_cast<long long>(static_cast<double>(L) * L / (2.0 * f));
     }
+    // Hits go out as candidate records (candidate.cpp:36-49), like `saw`: the half is the
+    // class prefix, then Gray(g) over positions [p, p+m) (bit set <=> -1), +1 elsewhere.
+    const int kp1 = (L + 1) / 2;
+    if (p < 1 || p > 30 || cls < 0 || cls >= (1 << (p - 1)) || m < 0 || p + m > kp1) {
+        std::cerr << "error: enumerate: bad --p / --class / --free for this length\n";
+        return 1;
+    }
+    std::vector<int8_t> prefixes((static_cast<size_t>(1) << (p - 1)) * static_cast<size_t>(p));
+    labs_rank_prefixes(p, prefixes.data());
     struct Ctx {
         std::ostream* out;
-        int L;
+        int L, kp1, p, m;
+        const int8_t* prefix;
+        std::vector<int8_t> half, full;
+        std::vector<char> line;
     };
     std::ofstream fo;
     std::ostream* out = &std::cout;
@@ -145,13 +157,22 @@ int cmd_enumerate(int argc, char** argv) {
         fo.open(v["--out"]);
         out = &fo;
     }
-    Ctx ctx{out, L};
+    Ctx ctx{out, L, kp1, p, m, &prefixes[static_cast<size_t>(cls) * static_cast<size_t>(p)],
+            std::vector<int8_t>(static_cast<size_t>(kp1)), std::vector<int8_t>(static_cast<size_t>(L)),
+            std::vector<char>(static_cast<size_t>(L) + 128)};
     labs_enum_stats st{};
     const int rc = labs_enumerate_class(
         L, p, cls, m, el, 0, 1ull << m,
         [](void* u, uint64_t g, int64_t e) -> int {
             auto* c = static_cast<Ctx*>(u);
-            *c->out << g << '\t' << e << '\n';
+            const uint64_t gray = g ^ (g >> 1);
+            for (int i = 0; i < c->kp1; ++i)
+                c->half[static_cast<size_t>(i)] =
+                    i < c->p ? c->prefix[i]
+                             : ((i < c->p + c->m && ((gray >> (i - c->p)) & 1)) ? int8_t(-1) : int8_t(1));
+            labs_expand_skew(c->half.data(), c->kp1, c->full.data());
+            labs_format_record(c->full.data(), c->L, e, c->line.data(), static_cast<int32_t>(c->line.size()));
+            *c->out << c->line.data() << '\n';
             return 0;
         },
         &ctx, &st);
