@@ -60,18 +60,28 @@ __device__ __forceinline__ int sbyte(uint32_t w, int b) {  // one PRMT, sign-rep
     return (int)r;
 }
 
-template <int NJ>
-__device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t chunk, int lane) {
+// One chunk of Gray codes per segment of LPW lanes (LPW = 16: two chunks per warp, the
+// per-step bookkeeping -- ctz, addresses, the flip stores, loop control -- serves both).
+template <int NJ, int LPW>
+__device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t chunk,
+                           bool valid, int sl) {
     const int L = P.L, k = P.k;
     const uint64_t g0 = P.g_begin + (chunk << P.chunk_log2);
     uint64_t g1 = g0 + (1ull << P.chunk_log2);
-    if (g1 > P.g_end || g1 < g0) g1 = P.g_end;
+    if (!valid) g1 = g0 + 1;  // (an idle segment: no steps)
+    if (g1 > P.g_end || g1 < g0) g1 = P.g_end > g0 ? P.g_end : g0 + 1;
     uint32_t* X0w = reinterpret_cast<uint32_t*>(X0);
     uint32_t* X1w = reinterpret_cast<uint32_t*>(X1);
+    auto seg_sum = [](int v) {
+        if (LPW == 32) return __reduce_add_sync(FULLMASK, v);
+#pragma unroll
+        for (int o = LPW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o, LPW);
+        return v;
+    };
 
     // ---- configuration g0: half = base with Gray(g0) over [p, p+m) negated ----
     const uint64_t gray0 = g0 ^ (g0 >> 1);
-    for (int wi = lane; wi < 2 * P.xwords; wi += 32) {
+    for (int wi = sl; wi < 2 * P.xwords; wi += LPW) {
         const int par = wi >= P.xwords;
         const int word = wi - par * P.xwords;
         uint32_t v = 0;
@@ -104,7 +114,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     for (int j = 0; j < NJ; ++j) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int t = 4 * (lane + 32 * j) + 1 + b;
+            const int t = 4 * (sl + LPW * j) + 1 + b;
             int acc = 0;
             if (t <= k) {
                 const int dw = t >> 2;
@@ -118,13 +128,11 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             e_part += acc * acc;
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e_part += __shfl_xor_sync(FULLMASK, e_part, o);
-    int energy = e_part;
+    int energy = seg_sum(e_part);
 
     int best_e = energy;
     uint64_t best_g = g0;
-    if (energy < P.e_l && lane == 0) {
+    if (valid && energy < P.e_l && sl == 0) {
         const unsigned long long slot = atomicAdd(P.rec_count, 1ull);
         if ((long long)slot < P.rec_cap) {
             uint32_t* r = P.rec + 4 * slot;
@@ -135,18 +143,26 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
         }
     }
 
-    // ---- Gray steps g = g0+1 .. g1-1 in batches of 32 ----
+    // ---- Gray steps g = g0+1 .. g1-1 in batches of LPW ----
     // ctz(g0 + i) = ctz(i) when the chunk start is a multiple of 2^chunk_log2 (every chunk
     // when g_begin is aligned); else the 64-bit path.
     const bool aligned = (g0 & ((1ull << P.chunk_log2) - 1)) == 0;
     const uint64_t nsteps = g1 - g0 - 1;
-    for (uint64_t s0 = 0; s0 < nsteps; s0 += 32) {
-        const int nb = (int)(nsteps - s0 < 32 ? nsteps - s0 : 32);
-        int mine = 0;  // dE of step s0 + lane (REDUX result of step `lane`)
-        for (int s = 0; s < nb; ++s) {  // (rolled: small code, no instruction-cache misses)
+    uint64_t nmax = nsteps;  // warp-uniform bound
+#pragma unroll
+    for (int o = LPW; o < 32; o <<= 1) {
+        const uint64_t other = __shfl_xor_sync(FULLMASK, (unsigned long long)nmax, o);
+        nmax = other > nmax ? other : nmax;
+    }
+    for (uint64_t s0 = 0; s0 < nmax; s0 += LPW) {
+        const int nb = (int)(nsteps > s0 ? (nsteps - s0 < LPW ? nsteps - s0 : LPW) : 0);
+        const int nbw = (int)(nmax - s0 < LPW ? nmax - s0 : LPW);
+        int mine = 0;  // dE of step s0 + sl
+        for (int s = 0; s < nbw; ++s) {  // (rolled: small code, no instruction-cache misses)
+            const bool live = s < nb;
             const uint64_t i = s0 + s + 1;
             const int tz = aligned ? __ffs((unsigned)i) - 1 : __ffsll((long long)(g0 + i)) - 1;
-            const int a = P.p + tz;
+            const int a = live ? P.p + tz : P.p;  // (idle: any valid position, no writes)
             const int ah = a >> 1;
             int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
             const uint32_t* Xaw = (a & 1) ? X1w : X0w;
@@ -154,7 +170,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             const bool cen = a == k;
             const int tstar = cen ? -3 : k - a;  // (-3: matches no lag word)
             const int xb = ((k - a) & 1) ? -xa : xa;
-            const int mul = cen ? -2 * xa : -4 * xa;
+            const int mul = live ? (cen ? -2 * xa : -4 * xa) : 0;
             const int awF = (P.xoff + ah + 1) >> 2;
             const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
             const int awB = (P.xoff + ah - 4) >> 2;
@@ -164,7 +180,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             int acc = 0;
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
-                const int sw = lane + 32 * j;
+                const int sw = sl + LPW * j;
                 if (sw < P.S) {  // lanes past the lag range read nothing
                     uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
                     const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
@@ -178,36 +194,38 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
                     }
                 }
             }
-            const int tot = __reduce_add_sync(FULLMASK, acc);
-            if (lane == s) mine = tot;
+            const int tot = seg_sum(acc);
+            if (sl == s) mine = tot;
             __syncwarp();
-            if (lane == 0) Xa[ah] = (int8_t)(-xa);
-            if (lane == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
+            if (live && sl == 0) Xa[ah] = (int8_t)(-xa);
+            if (live && sl == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
             __syncwarp();
         }
-        int e = mine;  // dE of step s0 + lane
+        int e = mine;  // dE of step s0 + sl
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULLMASK, e, o);
-            if (lane >= o) e += y;
+        for (int o = 1; o < LPW; o <<= 1) {
+            const int y = __shfl_up_sync(FULLMASK, e, o, LPW);
+            if (sl >= o) e += y;
         }
-        const bool valid = s0 + lane < nsteps;
+        const bool vstep = sl < nb;
         const int e_mine = energy + e;
-        const uint64_t g_mine = g0 + 1 + s0 + lane;
-        energy = __shfl_sync(FULLMASK, e_mine, 31);  // all 32 steps valid unless last batch
-        if (s0 + 32 > nsteps) energy = __shfl_sync(FULLMASK, e_mine, (int)(nsteps - s0 - 1));
-        if (valid && e_mine < best_e) {
+        const uint64_t g_mine = g0 + 1 + s0 + sl;
+        const int e_last = __shfl_sync(FULLMASK, e_mine, nb > 0 ? nb - 1 : 0, LPW);
+        if (nb > 0) energy = e_last;
+        if (vstep && e_mine < best_e) {
             best_e = e_mine;
             best_g = g_mine;
         }
-        const bool hit = valid && e_mine < P.e_l;
+        const bool hit = vstep && e_mine < P.e_l;
         const unsigned hm = __ballot_sync(FULLMASK, hit);
         if (hm) {
+            const int base_lane = (threadIdx.x & 31) - sl;
+            const unsigned seg_hm = (hm >> base_lane) & (LPW == 32 ? 0xffffffffu : ((1u << LPW) - 1u));
             unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(P.rec_count, (unsigned long long)__popc(hm));
-            base = __shfl_sync(FULLMASK, base, 0);
+            if (sl == 0 && seg_hm) base = atomicAdd(P.rec_count, (unsigned long long)__popc(seg_hm));
+            base = __shfl_sync(FULLMASK, base, 0, LPW);
             if (hit) {
-                const unsigned long long slot = base + __popc(hm & ((1u << lane) - 1));
+                const unsigned long long slot = base + __popc(seg_hm & ((1u << sl) - 1));
                 if ((long long)slot < P.rec_cap) {
                     uint32_t* r = P.rec + 4 * slot;
                     r[0] = (uint32_t)g_mine;
@@ -220,30 +238,35 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     }
     // chunk best: lowest E, then lowest g
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const int oe = __shfl_xor_sync(FULLMASK, best_e, o);
-        const unsigned long long og = __shfl_xor_sync(FULLMASK, (unsigned long long)best_g, o);
+    for (int o = LPW / 2; o > 0; o >>= 1) {
+        const int oe = __shfl_xor_sync(FULLMASK, best_e, o, LPW);
+        const unsigned long long og = __shfl_xor_sync(FULLMASK, (unsigned long long)best_g, o, LPW);
         if (oe < best_e || (oe == best_e && og < best_g)) {
             best_e = oe;
             best_g = og;
         }
     }
-    if (lane == 0) {
+    if (valid && sl == 0) {
         P.chunk_best[2 * chunk] = best_e;
         P.chunk_best[2 * chunk + 1] = (int64_t)best_g;
     }
     __syncwarp();
 }
 
-template <int NJ>
+template <int NJ, int LPW>
 __global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P) {
     extern __shared__ uint32_t esmem[];
+    constexpr int SEGS = 32 / LPW;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int8_t* X0 = reinterpret_cast<int8_t*>(esmem + warp * P.warp_words);
+    const int seg = lane / LPW, sl = lane % LPW;
+    int8_t* X0 = reinterpret_cast<int8_t*>(esmem + (warp * SEGS + seg) * P.warp_words);
     int8_t* X1 = X0 + 4 * P.xwords;
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t c = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < P.nchunks; c += nwarps)
-        enum_chunk<NJ>(P, X0, X1, c, lane);
+    const uint64_t ngrp = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t grp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; grp * SEGS < P.nchunks;
+         grp += ngrp) {
+        const uint64_t c = grp * SEGS + seg;
+        enum_chunk<NJ, LPW>(P, X0, X1, c < P.nchunks ? c : 0, c < P.nchunks, sl);
+    }
 }
 
 namespace {
@@ -362,17 +385,30 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         P.rec_count = cnt.p;
         P.chunk_best = best.p;
         cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), stream);
-        const size_t smem = static_cast<size_t>(4) * P.warp_words * 4;
+        // 16 lanes per chunk (two chunks per warp) while a lane owns <= 4 lag words
+        const int lpw = P.S <= 64 ? 16 : 32;
+        const int segs = 32 / lpw;
+        const size_t smem = static_cast<size_t>(4) * segs * P.warp_words * 4;
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        const uint64_t want = (P.nchunks + 3) / 4;
+        const uint64_t want = (P.nchunks + 4 * segs - 1) / (4 * segs);
         const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sms) * 8));
+        const int nj = (P.S + lpw - 1) / lpw;
         cudaEventRecord(e0, stream);
-        switch (P.nj) {
-            case 1: enum_kernel<1><<<grid, 128, smem, stream>>>(P); break;
-            case 2: enum_kernel<2><<<grid, 128, smem, stream>>>(P); break;
-            case 3: enum_kernel<3><<<grid, 128, smem, stream>>>(P); break;
-            default: enum_kernel<4><<<grid, 128, smem, stream>>>(P); break;
+        if (lpw == 16) {
+            switch (nj) {
+                case 1: enum_kernel<1, 16><<<grid, 128, smem, stream>>>(P); break;
+                case 2: enum_kernel<2, 16><<<grid, 128, smem, stream>>>(P); break;
+                case 3: enum_kernel<3, 16><<<grid, 128, smem, stream>>>(P); break;
+                default: enum_kernel<4, 16><<<grid, 128, smem, stream>>>(P); break;
+            }
+        } else {
+            switch (nj) {
+                case 1: enum_kernel<1, 32><<<grid, 128, smem, stream>>>(P); break;
+                case 2: enum_kernel<2, 32><<<grid, 128, smem, stream>>>(P); break;
+                case 3: enum_kernel<3, 32><<<grid, 128, smem, stream>>>(P); break;
+                default: enum_kernel<4, 32><<<grid, 128, smem, stream>>>(P); break;
+            }
         }
         cudaEventRecord(e1, stream);
         ce = cudaGetLastError();
