@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <string>
 #include <vector>
@@ -385,8 +386,12 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         P.rec_count = cnt.p;
         P.chunk_best = best.p;
         cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), stream);
-        // 16 lanes per chunk (two chunks per warp) while a lane owns <= 4 lag words
-        const int lpw = P.S <= 64 ? 16 : 32;
+        // 8 or 16 lanes per chunk (four or two chunks per warp) while a lane owns <= 4 lag
+        // words; LABS_ENUM_LPW=8|16|32 forces a width (A/B timing)
+        const char* lenv = std::getenv("LABS_ENUM_LPW");
+        const int lwant = lenv ? std::atoi(lenv) : 0;
+        int lpw = P.S <= 32 ? 8 : (P.S <= 64 ? 16 : 32);
+        if (lwant == 32 || (lwant == 16 && P.S <= 64) || (lwant == 8 && P.S <= 32)) lpw = lwant;
         const int segs = 32 / lpw;
         const size_t smem = static_cast<size_t>(4) * segs * P.warp_words * 4;
         int sms = 0;
@@ -395,7 +400,14 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sms) * 8));
         const int nj = (P.S + lpw - 1) / lpw;
         cudaEventRecord(e0, stream);
-        if (lpw == 16) {
+        if (lpw == 8) {
+            switch (nj) {
+                case 1: enum_kernel<1, 8><<<grid, 128, smem, stream>>>(P); break;
+                case 2: enum_kernel<2, 8><<<grid, 128, smem, stream>>>(P); break;
+                case 3: enum_kernel<3, 8><<<grid, 128, smem, stream>>>(P); break;
+                default: enum_kernel<4, 8><<<grid, 128, smem, stream>>>(P); break;
+            }
+        } else if (lpw == 16) {
             switch (nj) {
                 case 1: enum_kernel<1, 16><<<grid, 128, smem, stream>>>(P); break;
                 case 2: enum_kernel<2, 16><<<grid, 128, smem, stream>>>(P); break;
