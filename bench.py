@@ -195,7 +195,10 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group(backend="nccl" if args.impl == "b200" else "gloo")
+        # BENCH_DIST_BACKEND / BENCH_SAME_DEVICE: functional test of the N-rank flow on a
+        # one-GPU box (all ranks on device 0, gloo); the driver's runs use neither
+        backend = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if args.impl == "b200" else "gloo")
+        dist.init_process_group(backend=backend)
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
         if dist is not None:
@@ -207,6 +210,8 @@ def main():
     import paper_2409_07222_b200 as labs
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    if os.environ.get("BENCH_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
 
     walkers = args.walkers_per_gpu * ws
