@@ -175,15 +175,19 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.kp1 = wp.k + 1;
     wp.p = p;
     const int free_bits = wp.kp1 - p;
-    // lanes per walk: 16 (two walks per warp) while a lane's share of the neighbours stays
-    // within R <= 14 (the 3-blocks-per-SM register budget), else 32.  Measured on B200:
-    // L=101 1.6x, L=451 1.05x faster at 16; L=527 (R=16) faster at 32.
+    // lanes per walk: 8 (four walks per warp) while R <= 12, 16 (two walks) while R <= 14
+    // (the 3-blocks-per-SM register budget), else 32.  Measured on B200 (65,536 walks):
+    // L=101 19.3 / 12.1 / 8.8 ms at 32 / 16 / 8 lanes; L=201 92.7 / 70.4 / 64.9;
+    // L=451 210 / 191 (16); L=527 (R=16 at 16 lanes) faster at 32.
     // LABS_LPW=16|32 forces a width (A/B timing, tests).
     const char* lpw_env = std::getenv("LABS_LPW");
     const int lpw_want = lpw_force ? lpw_force : (lpw_env ? std::atoi(lpw_env) : 0);
     // (16-lane segments need bloom_k <= 16: one Bloom index per lane)
     const bool fit16 = (free_bits + 15) / 16 <= (lpw_want == 16 ? kMaxR : 14) && bloom_k <= 16;
-    wp.lpw = (lpw_want == 32 || !fit16) ? 32 : 16;
+    const bool fit8 = (free_bits + 7) / 8 <= (lpw_want == 8 ? kMaxR : 12) && bloom_k <= 16;
+    if (lpw_want == 32 || !fit16) wp.lpw = 32;
+    else if (fit8 && lpw_want != 16) wp.lpw = 8;  // (4 walks per warp, small lengths)
+    else wp.lpw = 16;
     wp.R = std::max(1, (free_bits + wp.lpw - 1) / wp.lpw);
     if (wp.R > kMaxR) return "saw: more than 512 free half bits is not supported by the GPU path";
     wp.S = std::max(1, (wp.k + 3) / 4);
@@ -226,7 +230,7 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     const int segs = 32 / wp.lpw;
     int wpb = 4;
     while (wpb > 1 && (fm_words + wpb * segs * wp.warp_words) * 4 > 227 * 1024) --wpb;
-    if ((fm_words + wpb * segs * wp.warp_words) * 4 > 227 * 1024 && wp.lpw == 16) {
+    if ((fm_words + wpb * segs * wp.warp_words) * 4 > 227 * 1024 && wp.lpw < 32) {
         wp.lpw = 32;  // two walks' state does not fit a block: one walk per warp
         return make_walk_params_impl(L, p, t_i, e_l, bloom_bits, bloom_k, wp, 32);
     }

@@ -78,10 +78,11 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
                             int* corr_out) {
     const size_t smem = walk_smem_bytes(P);
     const bool count = P.count_visited != 0;
-    switch (P.R * (P.lpw == 16 ? -1 : 1)) {
+    switch (P.R * (P.lpw == 16 ? -1 : 1) + (P.lpw == 8 ? 1000 : 0)) {
 #define LABS_CASE(r)                                                                   \
     case r: return launch_walk_fixed<r, 32>(P, grid, smem, st, score_out, corr_out, count); \
-    case -r: return launch_walk_fixed<r, 16>(P, grid, smem, st, score_out, corr_out, count);
+    case -r: return launch_walk_fixed<r, 16>(P, grid, smem, st, score_out, corr_out, count); \
+    case 1000 + r: return launch_walk_fixed<r, 8>(P, grid, smem, st, score_out, corr_out, count);
         LABS_CASE(1) LABS_CASE(2) LABS_CASE(3) LABS_CASE(4) LABS_CASE(5) LABS_CASE(6)
         LABS_CASE(7) LABS_CASE(8) LABS_CASE(9) LABS_CASE(10) LABS_CASE(11) LABS_CASE(12)
         LABS_CASE(13) LABS_CASE(14) LABS_CASE(15) LABS_CASE(16)
@@ -92,10 +93,11 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
 
 int walk_blocks_per_sm(const WalkParams& P) {
     const size_t smem = walk_smem_bytes(P);
-    switch (P.R * (P.lpw == 16 ? -1 : 1)) {
+    switch (P.R * (P.lpw == 16 ? -1 : 1) + (P.lpw == 8 ? 1000 : 0)) {
 #define LABS_CASE(r)                                 \
     case r: return blocks_per_sm_fixed<r, 32>(P, smem); \
-    case -r: return blocks_per_sm_fixed<r, 16>(P, smem);
+    case -r: return blocks_per_sm_fixed<r, 16>(P, smem); \
+    case 1000 + r: return blocks_per_sm_fixed<r, 8>(P, smem);
         LABS_CASE(1) LABS_CASE(2) LABS_CASE(3) LABS_CASE(4) LABS_CASE(5) LABS_CASE(6)
         LABS_CASE(7) LABS_CASE(8) LABS_CASE(9) LABS_CASE(10) LABS_CASE(11) LABS_CASE(12)
         LABS_CASE(13) LABS_CASE(14) LABS_CASE(15) LABS_CASE(16)

@@ -506,7 +506,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         // For L <= 1001, |dE| < 2^22 and one unsigned key (dE + 2^22) << 9 | a orders
         // (delta, hp) lexicographically, so one segment minimum finds the winner.
         int dstar = 0, astar = -1;
-        uint32_t ins_idx = 0;  // Bloom bit of the accepted neighbour, reused for the insert
+        uint32_t ins_idx = 0, ins_idx2 = 0;  // Bloom bits of the accepted neighbour (insert)
         uint32_t bkey = 0xffffffffu;
         int bd = INT_BIG, bm = 0;
         if (one_key) {  // pairwise (tree) minimum: log2(R) dependent steps, not R
@@ -548,11 +548,16 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const int mac = need ? ma : P.p;  // a safe index for segments not probing
             const uint64_t n1 = h1 ^ fm0[mac], n2 = h2 ^ fm1[mac];
             bool bit = true;
-            if (LPW >= 32 || sl < P.bloom_k) {  // one hash index per lane (bloom_k <= LPW)
+            if (LPW >= 32 || sl < P.bloom_k) {  // hash index sl (and sl + LPW for 8 lanes)
                 const uint32_t idx = bloom_index(n1, n2, sl, P.bloom_mu, P.bloom_bits);
                 if (sl < P.bloom_k) {
                     bit = (w.bloom[idx >> 5] >> (idx & 31)) & 1;
                     if (need) ins_idx = idx;  // kept for the insert if accepted
+                }
+                if (LPW < 16 && sl + LPW < P.bloom_k) {  // (bloom_k <= 2 LPW, host-checked)
+                    const uint32_t idx2 = bloom_index(n1, n2, sl + LPW, P.bloom_mu, P.bloom_bits);
+                    bit = bit && ((w.bloom[idx2 >> 5] >> (idx2 & 31)) & 1);
+                    if (need) ins_idx2 = idx2;
                 }
             }
             if (COUNT) {  // already filtered: the minimum is unvisited
@@ -611,6 +616,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             h2 ^= fm1[as];
             hf ^= fmf[as];
             if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
+            if (LPW < 16 && sl + LPW < P.bloom_k) atomicOr(&w.bloom[ins_idx2 >> 5], 1u << (ins_idx2 & 31));
             energy += dstar;
             best = min(best, energy);
         }
