@@ -219,13 +219,17 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.off_x1 = x1;
     wp.off_kl = wp.off_x1 + wp.xwords;
     wp.off_kh = wp.off_kl + wp.kwords;
-    wp.off_c16 = wp.off_kh + wp.kwords;
-    wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
-    wp.off_dc = wp.off_kq + round_up(wp.kp1, 4);
-    wp.off_half = wp.off_dc;  // (no per-lag dc array: T's C term reads the sequence)
+    wp.off_half = wp.off_kh + wp.kwords;
+    wp.off_dc = wp.off_half;  // (no per-lag dc array: T's C term reads the sequence)
     wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
-    wp.warp_words = wp.off_bloom + wp.bloom_words;
-    const int fm_words = round_up(3 * wp.kp1 * 2, 4);
+    // C16 and KQ are read only while the walk initialises its T registers, before the
+    // Bloom filter is cleared: they live inside the filter's words
+    wp.off_c16 = wp.off_bloom;
+    wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
+    const int init_words = 2 * round_up(wp.S, 4) + round_up(wp.kp1, 4);
+    wp.warp_words = wp.off_bloom + std::max(wp.bloom_words, init_words);
+    // the flip-mask table fm (3 kp1 u64, the same for every walk) is read through L1
+    const int fm_words = 0;
     wp.fm_words = fm_words;
     const int segs = 32 / wp.lpw;
     int wpb = 4;

@@ -86,76 +86,56 @@ __device__ __forceinline__ int sbyte(uint32_t w, int b) {  // one PRMT, sign-rep
 // Step w: X word w (positions 4w..4w+3 of the lane's parity) is shared by all R
 // neighbours; neighbour m needs kernel bytes koff + 4(w-m) - a0' .. +3, i.e. the
 // PRMT-aligned word KW_{w-m}; KW slides one slot per step (one new raw word).
-template <int R, bool WIDE>
+// acc[] accumulates onto its incoming value (the wide path runs the high-byte kernel
+// first, scales by 256 and continues with the low bytes in the same registers).
+template <int R>
 __device__ __forceinline__ void g_step(const uint32_t* __restrict__ Xw,
-                                       const uint32_t* __restrict__ Kl,
-                                       const uint32_t* __restrict__ Kh, int w, int j, int kb,
-                                       uint32_t sel, uint32_t (&KL)[R], uint32_t (&KH)[R],
-                                       uint32_t& rl, uint32_t& rh, int (&acc)[R],
-                                       int (&acch)[R]) {
+                                       const uint32_t* __restrict__ Kw, int w, int j, int kb,
+                                       uint32_t sel, uint32_t (&KW)[R], uint32_t& rw,
+                                       int (&acc)[R]) {
     const uint32_t x = Xw[w];
-    const uint32_t nl = Kl[kb + w + 2];
-    uint32_t nh = 0;
-    if (WIDE) nh = Kh[kb + w + 2];
+    const uint32_t nw = Kw[kb + w + 2];
 #pragma unroll
-    for (int m = 0; m < R; ++m) {
-        acc[m] = __dp4a((int)x, (int)KL[(j - m + R) % R], acc[m]);
-        if (WIDE) acch[m] = __dp4a((int)x, (int)KH[(j - m + R) % R], acch[m]);
-    }
-    KL[(j + 1) % R] = prmt(rl, nl, sel);
-    rl = nl;
-    if (WIDE) {
-        KH[(j + 1) % R] = prmt(rh, nh, sel);
-        rh = nh;
-    }
+    for (int m = 0; m < R; ++m) acc[m] = __dp4a((int)x, (int)KW[(j - m + R) % R], acc[m]);
+    KW[(j + 1) % R] = prmt(rw, nw, sel);
+    rw = nw;
 }
 
-template <int R, bool WIDE, int J>
+template <int R, int J>
 struct GTail {
     static __device__ __forceinline__ void run(const uint32_t* __restrict__ Xw,
-                                               const uint32_t* __restrict__ Kl,
-                                               const uint32_t* __restrict__ Kh, int w0, int rem,
-                                               int kb, uint32_t sel, uint32_t (&KL)[R],
-                                               uint32_t (&KH)[R], uint32_t& rl, uint32_t& rh,
-                                               int (&acc)[R], int (&acch)[R]) {
+                                               const uint32_t* __restrict__ Kw, int w0, int rem,
+                                               int kb, uint32_t sel, uint32_t (&KW)[R],
+                                               uint32_t& rw, int (&acc)[R]) {
         if (J < rem) {
-            g_step<R, WIDE>(Xw, Kl, Kh, w0 + J, J, kb, sel, KL, KH, rl, rh, acc, acch);
-            GTail<R, WIDE, J + 1>::run(Xw, Kl, Kh, w0, rem, kb, sel, KL, KH, rl, rh, acc, acch);
+            g_step<R>(Xw, Kw, w0 + J, J, kb, sel, KW, rw, acc);
+            GTail<R, J + 1>::run(Xw, Kw, w0, rem, kb, sel, KW, rw, acc);
         }
     }
 };
-template <int R, bool WIDE>
-struct GTail<R, WIDE, R> {
+template <int R>
+struct GTail<R, R> {
     static __device__ __forceinline__ void run(const uint32_t* __restrict__, const uint32_t* __restrict__,
-                                               const uint32_t* __restrict__, int, int, int,
-                                               uint32_t, uint32_t (&)[R], uint32_t (&)[R],
-                                               uint32_t&, uint32_t&, int (&)[R], int (&)[R]) {}
+                                               int, int, int, uint32_t, uint32_t (&)[R],
+                                               uint32_t&, int (&)[R]) {}
 };
 
-template <int R, bool WIDE>
+template <int R>
 __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
-                                             const uint32_t* __restrict__ Kl,
-                                             const uint32_t* __restrict__ Kh, int nwx, int kb,
-                                             uint32_t sel, int (&acc)[R], int (&acch)[R]) {
-    uint32_t KL[R], KH[R];
+                                             const uint32_t* __restrict__ Kw, int nwx, int kb,
+                                             uint32_t sel, int (&acc)[R]) {
+    uint32_t KW[R];
 #pragma unroll
-    for (int m = 0; m < R; ++m) {
-        KL[(R - m) % R] = prmt(Kl[kb - m], Kl[kb - m + 1], sel);
-        if (WIDE) KH[(R - m) % R] = prmt(Kh[kb - m], Kh[kb - m + 1], sel);
-        acc[m] = 0;
-        acch[m] = 0;
-    }
-    uint32_t rl = Kl[kb + 1], rh = 0;
-    if (WIDE) rh = Kh[kb + 1];
+    for (int m = 0; m < R; ++m) KW[(R - m) % R] = prmt(Kw[kb - m], Kw[kb - m + 1], sel);
+    uint32_t rw = Kw[kb + 1];
     const int nfull = (nwx / R) * R;
     for (int w0 = 0; w0 < nfull; w0 += R) {
 #pragma unroll
-        for (int j = 0; j < R; ++j)
-            g_step<R, WIDE>(Xw, Kl, Kh, w0 + j, j, kb, sel, KL, KH, rl, rh, acc, acch);
+        for (int j = 0; j < R; ++j) g_step<R>(Xw, Kw, w0 + j, j, kb, sel, KW, rw, acc);
     }
     // remainder steps j = 0 .. nwx - nfull - 1: nested guards, so a remainder of r costs
     // r + 1 tests instead of R
-    GTail<R, WIDE, 0>::run(Xw, Kl, Kh, nfull, nwx - nfull, kb, sel, KL, KH, rl, rh, acc, acch);
+    GTail<R, 0>::run(Xw, Kw, nfull, nwx - nfull, kb, sel, KW, rw, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -333,10 +313,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         (par ? w.X1w : w.X0w)[word] = v;
     }
     for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
-    {
-        uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
-        for (int i = sl; i < (P.bloom_words >> 2); i += LPW) b4[i] = make_uint4(0, 0, 0, 0);
-    }
     __syncwarp();
 
     // ---- exact C_{2t} of the owned lag words (registers), E, max|C| ----
@@ -411,6 +387,14 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         }
     }
 
+    // ---- clear the Bloom filter (it held C16 and KQ until here) ----
+    __syncwarp();
+    {
+        uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
+        for (int i = sl; i < (P.bloom_words >> 2); i += LPW) b4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
     // ---- half hashes h1, h2 (saw.cpp:77-89) and the initial Bloom insert ----
     uint64_t h1 = 0, h2 = 0;
     for (int i = sl; i < kp1; i += LPW) {
@@ -433,7 +417,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 
     const int e0 = energy;
     int best = energy;
-    long long iterations = 0, emitted = 0, probes = 0, wide_iters = 0, diverged = 0;
+    int iterations = 0, emitted = 0, wide_iters = 0, diverged = 0;  // each <= T_i < 2^28
+    long long probes = 0;  // (up to kp1 per iteration)
     long long evals_part = 0;  // per-lane unvisited-neighbour count (COUNT mode)
     int exhausted = 0;
     // lane-local neighbours excluded from the argmin: a > k (not neighbours) and the undo
@@ -458,21 +443,20 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         const bool cont = active && it < t_i32;
         if (!sg.uni(cont)) break;
         // ---- G for all owned neighbours (the O(L) part: IDP4A sliding dot product) ----
-        int acc[R], acch[R];
-        if (sg.uni(wide && cont)) {
-            g_neighbours<R, true>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
-        } else {
-            g_neighbours<R, false>(Xw, w.KL, w.KH, P.nwx, kb, ksel, acc, acch);
+        int acc[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) acc[m] = 0;
+        if (sg.uni(wide && cont)) {  // G = 256 G_high + G_low (a narrow segment passes zeros)
+            g_neighbours<R>(Xw, w.KH, P.nwx, kb, ksel, acc);
+#pragma unroll
+            for (int m = 0; m < R; ++m) acc[m] = wide ? acc[m] * 256 : 0;
         }
+        g_neighbours<R>(Xw, w.KL, P.nwx, kb, ksel, acc);
         if (wide && cont) ++wide_iters;
         // ---- exact deltas: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
-        for (int m = 0; m < R; ++m) {
-            // (acch = 0 from the narrow G loop; a non-wide segment in a wide warp ignores it)
-            const int gg = acc[m] + (wide ? 256 * acch[m] : 0);
-            delta[m] = T[m] - xs[m] * gg;
-        }
+        for (int m = 0; m < R; ++m) delta[m] = T[m] - xs[m] * acc[m];
         if (score_out) {
             if (valid)
 #pragma unroll
@@ -733,7 +717,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 #ifdef LABS_PHASE_CLOCKS
     if (walk < 4 && sl == 0 && valid)
         printf("[phase] walk %lld iters %lld  G %.0f  argmin+probe %.0f  apply %.0f cycles/iter\n",
-               (long long)walk, iterations, (double)ph_g / iterations, (double)ph_arg / iterations,
+               (long long)walk, (long long)iterations, (double)ph_g / iterations, (double)ph_arg / iterations,
                (double)ph_apply / iterations);
 #endif
 #undef LABS_PHASE
@@ -758,16 +742,18 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 // instead of spilling.
 template <int R, int LPW>
 struct MinBlocks {
+#ifdef LABS_MINB_OLD
     static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 3 : 2) : (R <= 12 ? 3 : 2));
+#else
+    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 2) : (R <= 12 ? 3 : 2));
+#endif
 };
 
 template <int R, int LPW, bool COUNT>
 __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
     saw_walk_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
-    uint64_t* fm = reinterpret_cast<uint64_t*>(smem_u4);
-    for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fm[i] = P.fm[i];
-    __syncthreads();
+    const uint64_t* __restrict__ fm = P.fm;  // (read-only, shared by all walks: L1-resident)
     constexpr int SEGS = Seg<LPW>::kSegs;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Seg<LPW> sg(lane);
