@@ -27,7 +27,7 @@ namespace labs_b200 {
 cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int* score_out,
                             int* corr_out);
 cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st);
-int walk_blocks_per_sm(const WalkParams& P);
+int walk_blocks_per_sm(WalkParams& P);  // (also places the fm table)
 
 namespace {
 thread_local std::string g_error;

@@ -228,7 +228,11 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
     const int init_words = 2 * round_up(wp.S, 4) + round_up(wp.kp1, 4);
     wp.warp_words = wp.off_bloom + std::max(wp.bloom_words, init_words);
-    // the flip-mask table fm (3 kp1 u64, the same for every walk) is read through L1
+    // walks of one warp (segments) sit warp_words apart: an odd multiple of 4 words puts
+    // their X0 / X1 words (read together in the G loop) in distinct banks for 2 or 4 segments
+    if (wp.warp_words % 8 == 0) wp.warp_words += 4;
+    // the flip-mask table fm (3 kp1 u64, the same for every walk) is read through L1 or
+    // copied per block; walk_blocks_per_sm decides, after the register budget is known
     const int fm_words = 0;
     wp.fm_words = fm_words;
     const int segs = 32 / wp.lpw;

@@ -91,7 +91,7 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
     }
 }
 
-int walk_blocks_per_sm(const WalkParams& P) {
+static int walk_blocks_for(const WalkParams& P) {
     const size_t smem = walk_smem_bytes(P);
     switch (P.R * (P.lpw == 16 ? -1 : 1) + (P.lpw == 8 ? 1000 : 0)) {
 #define LABS_CASE(r)                                 \
@@ -104,6 +104,20 @@ int walk_blocks_per_sm(const WalkParams& P) {
 #undef LABS_CASE
         default: return 0;
     }
+}
+
+// Resident blocks per SM, and where the flip-mask table fm lives: a per-block shared copy
+// (shortest probe latency) unless that copy costs a resident block, else read through L1.
+int walk_blocks_per_sm(WalkParams& P) {
+    P.fm_words = 0;
+    const int n_l1 = walk_blocks_for(P);
+    WalkParams Q = P;
+    Q.fm_words = (6 * P.kp1 + 3) / 4 * 4;
+    if (walk_blocks_for(Q) >= n_l1 && (Q.fm_words + Q.walks_per_block * Q.warp_words) * 4 <= 227 * 1024) {
+        P.fm_words = Q.fm_words;
+        return walk_blocks_for(Q);
+    }
+    return n_l1;
 }
 
 cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st) {

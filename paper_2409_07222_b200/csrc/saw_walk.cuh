@@ -745,7 +745,7 @@ struct MinBlocks {
 #ifdef LABS_MINB_OLD
     static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 3 : 2) : (R <= 12 ? 3 : 2));
 #else
-    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 2) : (R <= 12 ? 3 : 2));
+    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 3) : (R <= 16 ? 3 : 2));
 #endif
 };
 
@@ -753,7 +753,15 @@ template <int R, int LPW, bool COUNT>
 __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
     saw_walk_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
-    const uint64_t* __restrict__ fm = P.fm;  // (read-only, shared by all walks: L1-resident)
+    // flip-mask table: a block copy in shared memory, or (when that copy would cost a
+    // resident block) read through L1 -- P.fm_words decides (walk_blocks_per_sm)
+    const uint64_t* fm = P.fm;
+    if (P.fm_words) {
+        uint64_t* fs = reinterpret_cast<uint64_t*>(smem_u4);
+        for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fs[i] = P.fm[i];
+        __syncthreads();
+        fm = fs;
+    }
     constexpr int SEGS = Seg<LPW>::kSegs;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Seg<LPW> sg(lane);

@@ -1,8 +1,21 @@
+#!/bin/bash
+# A/B of the K1 register/occupancy policy: the in-tree build vs _lib_old (built with
+# EXTRA=-DLABS_MINB_OLD), over the BASELINE pool configs.  gpurun -- bash tools/ab_minblocks.sh
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_mb.log 2>&1; echo "pytest rc=$?"; tail -n 3 gpurun_out/pytest_mb.log
-for v in new old new old; do
-  if [ $v = old ]; then export LABS_B200_LIB=$PWD/paper_2409_07222_b200/_lib_old/libpaper_labs.so; else unset LABS_B200_LIB; fi
-  timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_mb_$v.log 2>&1
-  echo -n "$v: "; grep '^{' gpurun_out/bench_mb_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value %.4g  ms/step %.1f  frac %.3f  e2e %.4g launches %s' % (d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], d.get('gpu_launches')))"
+OLD=$PWD/paper_2409_07222_b200/_lib_old/libpaper_labs.so
+summ() { python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('  %-9s %8.2f ms  %.4g evals/s' % (d['config'], d['ms_per_pool'], d['flip_delta_evals_per_s']))"; }
+# VARIANTS: new (in-tree), old (_lib_old), lpw16 (in-tree, LABS_LPW=16), or any _lib_<name>
+for v in ${VARIANTS:-new old lpw16}; do
+  case $v in
+    old) export LABS_B200_LIB=$OLD; unset LABS_LPW;;
+    lpw16) unset LABS_B200_LIB; export LABS_LPW=16;;
+    new) unset LABS_B200_LIB LABS_LPW;;
+    *) export LABS_B200_LIB=$PWD/paper_2409_07222_b200/_lib_$v/libpaper_labs.so; unset LABS_LPW;;
+  esac
+  echo "$v:"; timeout 600 python tools/bench_configs.py --pools-only 2> gpurun_out/ab_$v.err | summ
 done

@@ -56,9 +56,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--m", type=int, default=36)
+    ap.add_argument("--pools-only", action="store_true", help="skip C2 (kernel-variant A/B)")
     a = ap.parse_args()
     res = [pool(*c) for c in POOLS]
-    res.insert(1, enum_c2(a.m))
+    if not a.pools_only:
+        res.insert(1, enum_c2(a.m))
     for r in res:
         print(json.dumps(r), flush=True)
     if a.out:
