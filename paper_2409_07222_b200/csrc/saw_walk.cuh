@@ -138,6 +138,22 @@ __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
     GTail<R, 0>::run(Xw, Kw, nfull, nwx - nfull, kb, sel, KW, rw, acc);
 }
 
+// Lane minimum of the (delta, hp) keys (dE + 2^22) * 512 + a over the neighbours not in
+// `skip`; pairwise (tree) minimum: log2(R) dependent steps, not R.
+template <int R>
+__device__ __forceinline__ uint32_t lane_min_key(const int (&delta)[R], uint32_t skip,
+                                                 uint32_t kbase) {
+    uint32_t key[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+        key[m] = (skip & (1u << m)) ? 0xffffffffu : (uint32_t)delta[m] * 512u + kbase + 8u * m;
+#pragma unroll
+    for (int h = 1; h < R; h <<= 1)
+#pragma unroll
+        for (int m = 0; m + h < R; m += 2 * h) key[m] = min(key[m], key[m + h]);
+    return key[0];
+}
+
 // ---------------------------------------------------------------------------
 struct WarpSmem {
     int8_t* X0;       // parity arrays (byte views, index xoff + i)
@@ -245,12 +261,24 @@ struct Seg {
     }
     __device__ __forceinline__ uint32_t umin(uint32_t v) const {
         if (LPW == 32) return __reduce_min_sync(FULLMASK, v);
+        if (LPW == 16) {  // two independent warp REDUX (one per half) instead of 4 shuffle levels
+            const bool hi = lane >= 16;
+            const uint32_t lo_min = __reduce_min_sync(FULLMASK, hi ? 0xffffffffu : v);
+            const uint32_t hi_min = __reduce_min_sync(FULLMASK, hi ? v : 0xffffffffu);
+            return hi ? hi_min : lo_min;
+        }
 #pragma unroll
         for (int o = LPW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o, LPW));
         return v;
     }
     __device__ __forceinline__ int imin(int v) const {
         if (LPW == 32) return __reduce_min_sync(FULLMASK, v);
+        if (LPW == 16) {
+            const bool hi = lane >= 16;
+            const int lo_min = __reduce_min_sync(FULLMASK, hi ? INT_BIG : v);
+            const int hi_min = __reduce_min_sync(FULLMASK, hi ? v : INT_BIG);
+            return hi ? hi_min : lo_min;
+        }
 #pragma unroll
         for (int o = LPW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o, LPW));
         return v;
@@ -493,16 +521,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         uint32_t ins_idx = 0, ins_idx2 = 0;  // Bloom bits of the accepted neighbour (insert)
         uint32_t bkey = 0xffffffffu;
         int bd = INT_BIG, bm = 0;
-        if (one_key) {  // pairwise (tree) minimum: log2(R) dependent steps, not R
-            uint32_t key[R];
-#pragma unroll
-            for (int m = 0; m < R; ++m)
-                key[m] = (skip & (1u << m)) ? 0xffffffffu : (uint32_t)delta[m] * 512u + kbase + 8u * m;
-#pragma unroll
-            for (int h = 1; h < R; h <<= 1)
-#pragma unroll
-                for (int m = 0; m + h < R; m += 2 * h) key[m] = min(key[m], key[m + h]);
-            bkey = key[0];
+        if (one_key) {
+            bkey = lane_min_key<R>(delta, skip, kbase);
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m)
@@ -557,17 +577,17 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             if (need && visited) {
                 if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
                     skip |= 1u << ((ma - a0) >> 3);
-                    bkey = 0xffffffffu;
-                    bd = INT_BIG;
-                    bm = 0;
+                    if (one_key) {
+                        bkey = lane_min_key<R>(delta, skip, kbase);
+                    } else {
+                        bd = INT_BIG;
+                        bm = 0;
 #pragma unroll
-                    for (int m = 0; m < R; ++m) {
-                        if (skip & (1u << m)) continue;
-                        bkey = min(bkey, (uint32_t)delta[m] * 512u + kbase + 8u * m);
-                        if (delta[m] < bd) {
-                            bd = delta[m];
-                            bm = m;
-                        }
+                        for (int m = 0; m < R; ++m)
+                            if (!(skip & (1u << m)) && delta[m] < bd) {
+                                bd = delta[m];
+                                bm = m;
+                            }
                     }
                 }
             } else if (need) {
