@@ -107,7 +107,8 @@ typedef struct labs_pool_stats {
     int64_t delta_evals_computed; /* deltas the GPU actually computed */
     int64_t exhausted_walks;
     int64_t wide_iterations;   /* iterations on the int16-correlation path */
-    double kernel_ms;          /* device time of the walk kernels (CUDA events) */
+    double kernel_ms;          /* device time of the walk kernels (CUDA events, summed over
+                                  batches; one device overlaps consecutive batches) */
     double seed_ms;            /* device time of the seed kernels */
     int32_t n_gpus;
     int32_t _pad;

@@ -181,7 +181,7 @@ public:
         LABS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int bps = std::max(1, walk_blocks_per_sm(wp));
         grid_cap = sms * bps;
-        rec_count.reserve(1);
+        rec_count.reserve(2);  // [0] records emitted, [1] the kernel's walk-group queue
     }
 
     // Generate halves for the segments on the device (K3).
@@ -250,33 +250,48 @@ public:
 
     // Run K1 over `nwalks` walks whose halves are resident; copy back records + stats.
     void walk(int64_t nwalks, BatchOut& out, int* score_out = nullptr, int* corr_out = nullptr) {
+        walk_launch(nwalks, score_out, corr_out);
+        walk_finish(nwalks, out, score_out, corr_out);
+    }
+
+    // Enqueue K1 and the drains of the record count and the per-walk stats on this
+    // runner's stream, without waiting (the pipelined pool overlaps the host replay of
+    // the previous batch with it).
+    void walk_launch(int64_t nwalks, int* score_out = nullptr, int* corr_out = nullptr) {
         stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
         if (rec_cap == 0) {
             rec_cap = std::max<int64_t>(1 << 16, 2 * nwalks);
             rec.reserve(static_cast<size_t>(rec_cap) * wp.rec_words);
         }
+        WalkParams P = wp;
+        P.nwalks = nwalks;
+        P.halves = halves.p;
+        P.rec = rec.p;
+        P.rec_cap = rec_cap;
+        P.rec_count = rec_count.p;
+        P.walk_next = rec_count.p + 1;
+        P.walk_stats = stats.p;
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(grid_cap, (nwalks + P.walks_per_block - 1) / P.walks_per_block)));
+        LABS_CUDA(cudaMemsetAsync(rec_count.p, 0, 2 * sizeof(unsigned long long), st));
+        LABS_CUDA(cudaEventRecord(ev[0], st));
+        LABS_CUDA(launch_saw_walk(P, grid, st, score_out, corr_out));
+        LABS_CUDA(cudaEventRecord(ev[1], st));
+        h_count.reserve(1);
+        LABS_CUDA(cudaMemcpyAsync(h_count.p, rec_count.p, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, st));
+        // the per-walk stats do not depend on the record count: drain them meanwhile
+        h_stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
+        LABS_CUDA(cudaMemcpyAsync(h_stats.p, stats.p,
+                                  static_cast<size_t>(nwalks) * kWalkStatWords * 8,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+
+    // Wait for the launch, copy back records + stats; a record-buffer overflow grows the
+    // buffer and reruns the (deterministic) walks.
+    void walk_finish(int64_t nwalks, BatchOut& out, int* score_out = nullptr, int* corr_out = nullptr) {
         for (int attempt = 0; attempt < 3; ++attempt) {
-            WalkParams P = wp;
-            P.nwalks = nwalks;
-            P.halves = halves.p;
-            P.rec = rec.p;
-            P.rec_cap = rec_cap;
-            P.rec_count = rec_count.p;
-            P.walk_stats = stats.p;
-            const int grid = static_cast<int>(std::max<int64_t>(
-                1, std::min<int64_t>(grid_cap, (nwalks + P.walks_per_block - 1) / P.walks_per_block)));
-            LABS_CUDA(cudaMemsetAsync(rec_count.p, 0, sizeof(unsigned long long), st));
-            LABS_CUDA(cudaEventRecord(ev[0], st));
-            LABS_CUDA(launch_saw_walk(P, grid, st, score_out, corr_out));
-            LABS_CUDA(cudaEventRecord(ev[1], st));
-            h_count.reserve(1);
-            LABS_CUDA(cudaMemcpyAsync(h_count.p, rec_count.p, sizeof(unsigned long long),
-                                      cudaMemcpyDeviceToHost, st));
-            // the per-walk stats do not depend on the record count: drain them meanwhile
-            h_stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
-            LABS_CUDA(cudaMemcpyAsync(h_stats.p, stats.p,
-                                      static_cast<size_t>(nwalks) * kWalkStatWords * 8,
-                                      cudaMemcpyDeviceToHost, st));
+            if (attempt > 0) walk_launch(nwalks, score_out, corr_out);
             LABS_CUDA(cudaStreamSynchronize(st));
             const unsigned long long cnt = *h_count.p;
             float ms = 0;
@@ -538,6 +553,7 @@ std::vector<uint32_t> walker_list(const labs_saw_config& cfg, const Derived& d, 
 }
 
 constexpr int64_t kMaxBatchWalks = 1 << 20;
+constexpr int64_t kPipelineBatches = 8;  // single-device pool: batches per call (at least 2 waves each)
 
 int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_batch_fn emit_batch,
              void* user, labs_pool_stats* out) {
@@ -629,53 +645,64 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
             std::vector<std::vector<BatchOut>> outs(static_cast<size_t>(ngpu));
             std::vector<std::vector<std::vector<Segment>>> segs_all(static_cast<size_t>(ngpu));
             std::vector<std::string> errs(static_cast<size_t>(ngpu));
+            // batches: whole walkers while they fit, else restart ranges
+            const auto make_batches = [&](const std::vector<uint32_t>& wl, int64_t max_walks) {
+                std::vector<std::vector<Segment>> batches;
+                std::vector<Segment> cur;
+                int64_t cur_walks = 0;
+                for (uint32_t w : wl) {
+                    int64_t r = 0;
+                    while (r < R) {
+                        const int64_t take = std::min(R - r, max_walks - cur_walks);
+                        cur.push_back(Segment{w, r, r + take});
+                        cur_walks += take;
+                        r += take;
+                        if (cur_walks == max_walks) {
+                            batches.push_back(std::move(cur));
+                            cur.clear();
+                            cur_walks = 0;
+                        }
+                    }
+                }
+                if (!cur.empty()) batches.push_back(std::move(cur));
+                return batches;
+            };
+            // Seed one batch on `dr` (K3); a walker split across batches continues from the
+            // generator state its previous batch ended with.
+            struct Carry {
+                uint32_t walker = 0xffffffffu;
+                std::array<uint64_t, 4> state{};
+            };
+            const auto seed_batch = [&](DeviceRunner& dr, const std::vector<Segment>& segs, Carry& carry,
+                                        BatchOut& b) {
+                std::vector<std::array<uint64_t, 4>> states(segs.size());
+                std::vector<int32_t> init(segs.size(), 1);
+                int64_t nw = 0;
+                for (size_t i = 0; i < segs.size(); ++i) {
+                    if (segs[i].r0 > 0 && segs[i].walker == carry.walker) {
+                        init[i] = 0;
+                        states[i] = carry.state;
+                    }
+                    for (int64_t r = segs[i].r0; r < segs[i].r1; ++r) {
+                        b.walk_walker.push_back(segs[i].walker);
+                        b.walk_restart.push_back(r);
+                    }
+                    nw += segs[i].r1 - segs[i].r0;
+                }
+                dr.seed(segs, d, cfg.seed, states, init, nw, b);
+                carry.walker = segs.back().walker;
+                carry.state = states.back();
+                return nw;
+            };
             auto dev_job = [&](int g) {
                 try {
                     DeviceRunner& dr = *runners[static_cast<size_t>(g)];
                     LABS_CUDA(cudaSetDevice(dr.dev));
-                    const auto& wl = per_dev[static_cast<size_t>(g)];
-                    // batches: whole walkers while they fit, else restart ranges
-                    std::vector<Segment> cur;
-                    int64_t cur_walks = 0;
-                    std::vector<std::vector<Segment>> batches;
-                    for (uint32_t w : wl) {
-                        int64_t r = 0;
-                        while (r < R) {
-                            const int64_t take = std::min(R - r, kMaxBatchWalks - cur_walks);
-                            cur.push_back(Segment{w, r, r + take});
-                            cur_walks += take;
-                            r += take;
-                            if (cur_walks == kMaxBatchWalks) {
-                                batches.push_back(std::move(cur));
-                                cur.clear();
-                                cur_walks = 0;
-                            }
-                        }
-                    }
-                    if (!cur.empty()) batches.push_back(std::move(cur));
-                    std::vector<std::array<uint64_t, 4>> carry;  // state of a split walker
-                    uint32_t carry_w = 0xffffffffu;
-                    std::array<uint64_t, 4> carry_state{};
-                    for (auto& segs : batches) {
+                    Carry carry;
+                    for (auto& segs : make_batches(per_dev[static_cast<size_t>(g)], kMaxBatchWalks)) {
                         BatchOut b;
-                        std::vector<std::array<uint64_t, 4>> states(segs.size());
-                        std::vector<int32_t> init(segs.size(), 1);
-                        int64_t nw = 0;
-                        for (size_t i = 0; i < segs.size(); ++i) {
-                            if (segs[i].r0 > 0 && segs[i].walker == carry_w) {
-                                init[i] = 0;
-                                states[i] = carry_state;
-                            }
-                            for (int64_t r = segs[i].r0; r < segs[i].r1; ++r) {
-                                b.walk_walker.push_back(segs[i].walker);
-                                b.walk_restart.push_back(r);
-                            }
-                            nw += segs[i].r1 - segs[i].r0;
-                        }
                         const auto tA = std::chrono::steady_clock::now();
-                        dr.seed(segs, d, cfg.seed, states, init, nw, b);
-                        carry_w = segs.back().walker;
-                        carry_state = states.back();
+                        const int64_t nw = seed_batch(dr, segs, carry, b);
                         const auto tB = std::chrono::steady_clock::now();
                         dr.walk(nw, b);
                         const auto tC = std::chrono::steady_clock::now();
@@ -692,7 +719,49 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                 }
             };
             if (ngpu == 1) {
-                dev_job(0);
+                // One device: the walks run as a pipeline of batches on two runners (two
+                // streams and buffer sets).  While batch i runs -- and fills the SMs its
+                // predecessor's tail leaves idle -- the host replays batch i-1 into the sink.
+                runners.push_back(acquire_runner(first, wp));
+                DeviceRunner* slot[2] = {runners[0].get(), runners[1].get()};
+                LABS_CUDA(cudaSetDevice(slot[0]->dev));
+                const int64_t resident = static_cast<int64_t>(slot[0]->grid_cap) * wp.walks_per_block;
+                const int64_t total = static_cast<int64_t>(walkers.size()) * R;
+                const int64_t chunk = std::min<int64_t>(
+                    kMaxBatchWalks, std::max<int64_t>(2 * resident, (total + kPipelineBatches - 1) / kPipelineBatches));
+                const auto batches = make_batches(walkers, chunk);
+                std::vector<BatchOut> bo(batches.size());
+                std::vector<int64_t> nws(batches.size());
+                Carry carry;
+                const auto tD = std::chrono::steady_clock::now();
+                double replay_ms = 0;
+                const auto retire = [&](size_t j) {  // wait for batch j, replay it, free it
+                    slot[j % 2]->walk_finish(nws[j], bo[j]);
+                    acc.st.kernel_ms += bo[j].kernel_ms;
+                    acc.st.seed_ms += bo[j].seed_ms;
+                    acc.st.h2d_bytes += bo[j].h2d;
+                    acc.st.d2h_bytes += bo[j].d2h;
+                    const auto t = std::chrono::steady_clock::now();
+                    if (!sink.aborted && acc.diverged == 0) process_batch(batches[j], bo[j]);
+                    replay_ms += std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now() - t).count();
+                    bo[j] = BatchOut();
+                };
+                size_t launched = 0, retired = 0;
+                for (size_t i = 0; i < batches.size(); ++i) {
+                    if (i >= 2) retire(retired++);  // batch i - 2: frees slot i % 2
+                    if (sink.aborted || acc.diverged) break;
+                    nws[i] = seed_batch(*slot[i % 2], batches[i], carry, bo[i]);
+                    slot[i % 2]->walk_launch(nws[i]);
+                    launched = i + 1;
+                }
+                while (retired < launched) retire(retired++);
+                if (std::getenv("LABS_TIMING"))
+                    std::fprintf(stderr, "[labs] %zu pipelined batches of <= %lld walks: %.2f ms, "
+                                 "host replay %.2f ms (overlapped)\n", batches.size(),
+                                 static_cast<long long>(chunk),
+                                 std::chrono::duration<double, std::milli>(
+                                     std::chrono::steady_clock::now() - tD).count(), replay_ms);
             } else {
                 std::vector<std::thread> th;
                 for (int g = 0; g < ngpu; ++g) th.emplace_back(dev_job, g);
@@ -700,26 +769,18 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
             }
             for (const auto& e : errs)
                 if (!e.empty()) throw CudaFailure(e);
-            for (int g = 0; g < ngpu; ++g) {  // device time = slowest device
-                double kms = 0, sms = 0;
-                for (const auto& b : outs[static_cast<size_t>(g)]) {
-                    kms += b.kernel_ms;
-                    sms += b.seed_ms;
-                    acc.st.h2d_bytes += b.h2d;
-                    acc.st.d2h_bytes += b.d2h;
+            if (ngpu > 1) {
+                for (int g = 0; g < ngpu; ++g) {  // device time = slowest device
+                    double kms = 0, sms = 0;
+                    for (const auto& b : outs[static_cast<size_t>(g)]) {
+                        kms += b.kernel_ms;
+                        sms += b.seed_ms;
+                        acc.st.h2d_bytes += b.h2d;
+                        acc.st.d2h_bytes += b.d2h;
+                    }
+                    acc.st.kernel_ms = std::max(acc.st.kernel_ms, kms);
+                    acc.st.seed_ms = std::max(acc.st.seed_ms, sms);
                 }
-                acc.st.kernel_ms = std::max(acc.st.kernel_ms, kms);
-                acc.st.seed_ms = std::max(acc.st.seed_ms, sms);
-            }
-            if (ngpu == 1) {
-                const auto tD = std::chrono::steady_clock::now();
-                for (size_t bi = 0; bi < outs[0].size(); ++bi) process_batch(segs_all[0][bi], outs[0][bi]);
-                if (std::getenv("LABS_TIMING"))
-                    std::fprintf(stderr, "[labs] host replay %.2f ms, prep %.2f ms\n",
-                                 std::chrono::duration<double, std::milli>(
-                                     std::chrono::steady_clock::now() - tD).count(),
-                                 std::chrono::duration<double, std::milli>(tD - t0).count());
-            } else {
                 // merge: walks of all devices in (walker, restart) order
                 struct Ref {
                     uint32_t walker;

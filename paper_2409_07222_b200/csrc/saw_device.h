@@ -55,6 +55,7 @@ struct WalkParams {
     // outputs
     uint32_t* rec;                 // [rec_cap][rec_words]
     unsigned long long* rec_count; // emissions attempted (may exceed rec_cap => overflow)
+    unsigned long long* walk_next; // dynamic walk-group queue (zeroed per launch)
     int64_t* walk_stats;           // [nwalks][kWalkStatWords]
 };
 

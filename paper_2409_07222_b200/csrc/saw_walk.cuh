@@ -799,12 +799,17 @@ __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
     w.KQ = reinterpret_cast<int*>(base + P.off_kq);
     w.half = base + P.off_half;
     w.bloom = base + P.off_bloom;
-    const int64_t stride = (int64_t)gridDim.x * P.warps_per_block;
-    for (int64_t grp = (int64_t)blockIdx.x * P.warps_per_block + warp; grp * SEGS < P.nwalks;
-         grp += stride) {
+    // walk groups (one per warp: SEGS walks) are handed out dynamically -- walks differ in
+    // length (exhaustion, Bloom retries), so a static stride leaves SMs idle at the tail
+    const int64_t nwarps = (int64_t)gridDim.x * P.warps_per_block;
+    int64_t grp = (int64_t)blockIdx.x * P.warps_per_block + warp;
+    while (grp * SEGS < P.nwalks) {
         const int64_t walk = grp * SEGS + seg;
         run_walk_seg<R, LPW, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, walk < P.nwalks,
                                     sg, score_out, corr_out);
+        unsigned long long nx = 0;
+        if (lane == 0) nx = atomicAdd(P.walk_next, 1ull);
+        grp = nwarps + (int64_t)__shfl_sync(FULLMASK, nx, 0);
     }
 }
 
