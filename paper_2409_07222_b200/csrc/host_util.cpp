@@ -175,16 +175,17 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.kp1 = wp.k + 1;
     wp.p = p;
     const int free_bits = wp.kp1 - p;
-    // lanes per walk: 8 (four walks per warp) while R <= 12, 16 (two walks) while R <= 14
-    // (the 3-blocks-per-SM register budget), else 32.  Measured on B200 (65,536 walks):
-    // L=101 19.3 / 12.1 / 8.8 ms at 32 / 16 / 8 lanes; L=201 92.7 / 70.4 / 64.9;
-    // L=451 210 / 191 (16); L=527 (R=16 at 16 lanes) faster at 32.
-    // LABS_LPW=16|32 forces a width (A/B timing, tests).
+    // lanes per walk: the narrowest of 8 (four walks per warp), 16 (two walks) and 32 with
+    // R <= 16 neighbours per lane.  Measured on B200 (tools/lpw_sweep.py, 16,384 walks,
+    // flip-deltas/s at 8 / 16 / 32 lanes): L=101 1.23e11 / 0.96e11 / 0.58e11;
+    // L=251 1.66e11 / 1.61e11 / 1.19e11; L=401 - / 1.57e11 / 1.21e11;
+    // L=527 - / 1.39e11 / 1.30e11.
+    // LABS_LPW=8|16|32 forces a width (A/B timing, tests).
     const char* lpw_env = std::getenv("LABS_LPW");
     const int lpw_want = lpw_force ? lpw_force : (lpw_env ? std::atoi(lpw_env) : 0);
     // (16-lane segments need bloom_k <= 16: one Bloom index per lane)
-    const bool fit16 = (free_bits + 15) / 16 <= (lpw_want == 16 ? kMaxR : 14) && bloom_k <= 16;
-    const bool fit8 = (free_bits + 7) / 8 <= (lpw_want == 8 ? kMaxR : 12) && bloom_k <= 16;
+    const bool fit16 = (free_bits + 15) / 16 <= kMaxR && bloom_k <= 16;
+    const bool fit8 = (free_bits + 7) / 8 <= kMaxR && bloom_k <= 16;
     if (lpw_want == 32 || !fit16) wp.lpw = 32;
     else if (fit8 && lpw_want != 16) wp.lpw = 8;  // (4 walks per warp, small lengths)
     else wp.lpw = 16;
