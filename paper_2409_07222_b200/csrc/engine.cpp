@@ -727,8 +727,10 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                 LABS_CUDA(cudaSetDevice(slot[0]->dev));
                 const int64_t resident = static_cast<int64_t>(slot[0]->grid_cap) * wp.walks_per_block;
                 const int64_t total = static_cast<int64_t>(walkers.size()) * R;
+                const char* nb_env = std::getenv("LABS_PIPELINE_BATCHES");  // (A/B knob)
+                const int64_t nb = std::max<int64_t>(1, nb_env ? std::atoll(nb_env) : kPipelineBatches);
                 const int64_t chunk = std::min<int64_t>(
-                    kMaxBatchWalks, std::max<int64_t>(2 * resident, (total + kPipelineBatches - 1) / kPipelineBatches));
+                    kMaxBatchWalks, nb == 1 ? total : std::max<int64_t>(2 * resident, (total + nb - 1) / nb));
                 const auto batches = make_batches(walkers, chunk);
                 std::vector<BatchOut> bo(batches.size());
                 std::vector<int64_t> nws(batches.size());

@@ -5,7 +5,7 @@
 set -u
 TAG=${1:-r01}
 mkdir -p gpurun_out
-CMD="python tools/profile_walk.py 451 1024 4 0"
+CMD="python tools/profile_walk.py 451 1024 ${RESTARTS:-16} 0"  # 16,384 walks: every SM at full residency
 $CMD > gpurun_out/prof_plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:saw_walk_kernel -c 1 \
     -o gpurun_out/walk_$TAG -f $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
