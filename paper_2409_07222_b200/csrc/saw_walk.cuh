@@ -640,27 +640,28 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         //     changes (its only pair through a* is (a*, b*), both zeroed).
         const int mul = cen ? -2 * xa : -4 * xa;
         if (step) {
-            skip = inval;
+            // One convergent loop for both updates.  For a of a*'s parity the Q partner
+            // x_{2a-b*} is the C-term's x_{a*-2t} (2a - b* = a* - 2(k-a)), so three byte
+            // loads per neighbour serve both; lanes of the other parity take the Q part
+            // with zero factors instead of diverging.
             const int8_t* Xf = Xa + ah + (k - a0);  // x_{a*+2t}, t = k - a = (k - a0) - 8m
-            const int8_t* Xg = Xa + ah - (k - a0);  // x_{a*-2t}
+            const int8_t* Xg = Xa + ah - (k - a0);  // x_{a*-2t}  (= x_{2a-b*})
+            const int8_t* Xp = Xa + ((2 * a0 - as) >> 1);  // x_{2a-a*}
             const int cmul = sgn8 * mul;
+            const bool same = par == apar;  // (the owner of astar has astar's parity)
+            const int qa = same ? -64 * xa : 0, qb = same ? -64 * xb : 0;
+            const int ex3 = as + L - 1;  // == 3a for the pair excluded from Q(a)
+            // the pivot's own entry (undo move): no Q change, xs flips, skipped next step
+            const bool own_lane = same && dstar_l >= 0 && (dstar_l & 7) == 0 && dstar_l < 8 * R;
+            skip = inval | (own_lane ? 1u << (dstar_l >> 3) : 0u);
 #pragma unroll
-            for (int m = 0; m < R; ++m) T[m] += cmul * ((int)Xf[-8 * m] + (int)Xg[8 * m]);
-            if (par == apar) {  // (the owner of astar has astar's parity)
-                const int ex3 = as + L - 1;  // == 3a for the excluded pair
-                const int8_t* Xp = Xa + ((2 * a0 - as) >> 1);
-                const int8_t* Xq = Xa + ((2 * a0 - bstar) >> 1);
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    int xp = Xp[8 * m];
-                    const int xq = Xq[8 * m];
-                    if (3 * (a0 + 8 * m) == ex3) xp = 0;
-                    const int term = xa * xp + xb * xq;
-                    const bool own = dstar_l == 8 * m;  // the pivot's own entry (undo move)
-                    T[m] -= own ? 0 : 64 * term;
-                    xs[m] = own ? -xs[m] : xs[m];
-                    skip |= own ? (1u << m) : 0u;
-                }
+            for (int m = 0; m < R; ++m) {
+                const int f = Xf[-8 * m], g = Xg[8 * m];
+                int xp = Xp[8 * m];
+                if (3 * (a0 + 8 * m) == ex3) xp = 0;
+                const bool own = dstar_l == 8 * m;  // (x_{2a*-a*} = x_{a*} reads the zeroed 0)
+                T[m] += cmul * (f + g) + qa * xp + qb * (own ? 0 : g);
+                xs[m] = own ? -xs[m] : xs[m];
             }
         }
         // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
