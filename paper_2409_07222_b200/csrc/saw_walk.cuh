@@ -139,14 +139,13 @@ __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
 }
 
 // Lane minimum of the (delta, hp) keys (dE + 2^22) * 512 + a over the neighbours not in
-// `skip`; pairwise (tree) minimum: log2(R) dependent steps, not R.
+// `skip` (v[] holds the keys themselves: see the key-scaled T registers in run_walk_seg);
+// pairwise (tree) minimum: log2(R) dependent steps, not R.
 template <int R>
-__device__ __forceinline__ uint32_t lane_min_key(const int (&delta)[R], uint32_t skip,
-                                                 uint32_t kbase) {
+__device__ __forceinline__ uint32_t lane_min_key(const int (&v)[R], uint32_t skip) {
     uint32_t key[R];
 #pragma unroll
-    for (int m = 0; m < R; ++m)
-        key[m] = (skip & (1u << m)) ? 0xffffffffu : (uint32_t)delta[m] * 512u + kbase + 8u * m;
+    for (int m = 0; m < R; ++m) key[m] = (skip & (1u << m)) ? 0xffffffffu : (uint32_t)v[m];
 #pragma unroll
     for (int h = 1; h < R; h <<= 1)
 #pragma unroll
@@ -397,21 +396,31 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     const uint32_t ksel = sel4((P.koff - a0h) & 3);
     const int sgn8 = ((k - a0) & 1) ? -8 : 8;  // 8 (-1)^(k-a), the same for every m
     const uint32_t kbase = 0x80000000u + (uint32_t)a0;  // key = (dE + 2^22) * 512 + a
-    int T[R], xs[R];  // (meaningless for a > k: those are masked by `inval`)
+    // For L <= 1001, |dE| < 2^22 and the unsigned key (dE + 2^22) * 512 + a orders
+    // (delta, hp) lexicographically.  T and xs are then kept key-scaled,
+    //     T'(a) = 512 T(a) + 2^31 + a,   xs' = 512 xs,
+    // so that one IMAD, T' - xs' G, yields the key itself (wrapping mod 2^32 exactly like
+    // the unsigned key).  Longer lengths keep the plain delta (sc = 1).
+    const bool one_key = L <= 1001;
+    const int sc = one_key ? 512 : 1;
+    uint32_t T[R];  // (unsigned: the key form wraps mod 2^32; meaningless for a > k, masked)
+    int xs[R];
     {
         const int16_t* C16h = reinterpret_cast<const int16_t*>(w.C16);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int a = a0 + 8 * m;
-            T[m] = 0;
+            int t = 0;
             xs[m] = 0;
             if (a < k) {
-                T[m] = w.KQ[a] + sgn8 * (int)C16h[k - a - 1];
+                t = w.KQ[a] + sgn8 * (int)C16h[k - a - 1];
                 xs[m] = 8 * (int)Xmine[a >> 1];
             } else if (a == k) {
-                T[m] = w.KQ[a];
+                t = w.KQ[a];
                 xs[m] = 4 * (int)Xmine[a >> 1];
             }
+            T[m] = (uint32_t)(t * sc) + (one_key ? kbase + 8u * m : 0u);
+            xs[m] *= sc;
         }
     }
 
@@ -457,7 +466,6 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         if (a0 + 8 * m > k) inval |= 1u << m;
     uint32_t skip = inval;
     const int64_t t_i = score_out ? 1 : P.t_i;
-    const bool one_key = L <= 1001;
     bool active = valid;  // this segment's walk is still running
 
     const int t_i32 = (int)t_i;  // T_i < 2^28 (make_walk_params: Bloom bits < 2^32)
@@ -484,12 +492,15 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         // ---- exact deltas: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
-        for (int m = 0; m < R; ++m) delta[m] = T[m] - xs[m] * acc[m];
+        for (int m = 0; m < R; ++m)  // the key if one_key
+            delta[m] = (int)(T[m] - (uint32_t)xs[m] * (uint32_t)acc[m]);
         if (score_out) {
             if (valid)
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    if (a0 + 8 * m <= k) score_out[walk * kp1 + a0 + 8 * m] = delta[m];
+                    if (a0 + 8 * m <= k)
+                        score_out[walk * kp1 + a0 + 8 * m] =
+                            one_key ? (int)((uint32_t)delta[m] - kbase - 8u * m) >> 9 : delta[m];
             break;
         }
 
@@ -522,7 +533,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         uint32_t bkey = 0xffffffffu;
         int bd = INT_BIG, bm = 0;
         if (one_key) {
-            bkey = lane_min_key<R>(delta, skip, kbase);
+            bkey = lane_min_key<R>(delta, skip);
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m)
@@ -578,7 +589,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                 if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
                     skip |= 1u << ((ma - a0) >> 3);
                     if (one_key) {
-                        bkey = lane_min_key<R>(delta, skip, kbase);
+                        bkey = lane_min_key<R>(delta, skip);
                     } else {
                         bd = INT_BIG;
                         bm = 0;
@@ -647,9 +658,9 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const int8_t* Xf = Xa + ah + (k - a0);  // x_{a*+2t}, t = k - a = (k - a0) - 8m
             const int8_t* Xg = Xa + ah - (k - a0);  // x_{a*-2t}  (= x_{2a-b*})
             const int8_t* Xp = Xa + ((2 * a0 - as) >> 1);  // x_{2a-a*}
-            const int cmul = sgn8 * mul;
+            const int cmul = sgn8 * mul * sc;
             const bool same = par == apar;  // (the owner of astar has astar's parity)
-            const int qa = same ? -64 * xa : 0, qb = same ? -64 * xb : 0;
+            const int qa = same ? -64 * sc * xa : 0, qb = same ? -64 * sc * xb : 0;
             const int ex3 = as + L - 1;  // == 3a for the pair excluded from Q(a)
             // the pivot's own entry (undo move): no Q change, xs flips, skipped next step
             const bool own_lane = same && dstar_l >= 0 && (dstar_l & 7) == 0 && dstar_l < 8 * R;
@@ -660,7 +671,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                 int xp = Xp[8 * m];
                 if (3 * (a0 + 8 * m) == ex3) xp = 0;
                 const bool own = dstar_l == 8 * m;  // (x_{2a*-a*} = x_{a*} reads the zeroed 0)
-                T[m] += cmul * (f + g) + qa * xp + qb * (own ? 0 : g);
+                T[m] += (uint32_t)(cmul * (f + g) + qa * xp + qb * (own ? 0 : g));
                 xs[m] = own ? -xs[m] : xs[m];
             }
         }
