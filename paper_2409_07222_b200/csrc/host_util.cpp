@@ -199,8 +199,8 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.xoff = 4 * wp.S + 8;
     const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3)});
     wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
-    // kernel: main loop reads d in [-(p+32R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4S+4
-    const int amax_h = (p + 32 * wp.R) / 2 + 1;
+    // kernel: main loop reads d in [-(p+lpw R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4S+4
+    const int amax_h = (p + wp.lpw * wp.R) / 2 + 1;  // a0 + 8m < p + lpw R
     int koff = std::max(amax_h + 4 * wp.R + 12, 4 * wp.S + 12);
     while (koff % 4 != 3) ++koff;
     wp.koff = koff;
