@@ -210,11 +210,13 @@ __device__ __forceinline__ void store_c_word(const WarpSmem& w, const WalkParams
     w.C16[2 * s + 1] = prmt((uint32_t)c[2], (uint32_t)c[3], 0x5410);
     const int fw = (P.koff + 1) / 4 + s;
     const int bw = (P.koff - 3) / 4 - s;
-    w.KL[fw] = pack4(c[0], c[1], c[2], c[3]);
-    w.KL[bw] = pack4(c[2], c[1], c[0], cprev);
+    const uint32_t lo = pack4(c[0], c[1], c[2], c[3]);
+    w.KL[fw] = lo;
+    w.KL[bw] = prmt(lo, (uint32_t)cprev, 0x4012);  // (c2, c1, c0, cprev)
     if (wide) {
-        w.KH[fw] = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
-        w.KH[bw] = pack4(hi_byte(c[2]), hi_byte(c[1]), hi_byte(c[0]), hi_byte(cprev));
+        const uint32_t hi = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[fw] = hi;
+        w.KH[bw] = prmt(hi, (uint32_t)hi_byte(cprev), 0x4012);
     }
 }
 
@@ -223,11 +225,13 @@ __device__ __forceinline__ void store_k_word(const WarpSmem& w, const WalkParams
                                              const int (&c)[4], int cprev, bool wide) {
     const int fw = (P.koff + 1) / 4 + s;
     const int bw = (P.koff - 3) / 4 - s;
-    w.KL[fw] = pack4(c[0], c[1], c[2], c[3]);
-    w.KL[bw] = pack4(c[2], c[1], c[0], cprev);
+    const uint32_t lo = pack4(c[0], c[1], c[2], c[3]);
+    w.KL[fw] = lo;
+    w.KL[bw] = prmt(lo, (uint32_t)cprev, 0x4012);  // (c2, c1, c0, cprev)
     if (wide) {
-        w.KH[fw] = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
-        w.KH[bw] = pack4(hi_byte(c[2]), hi_byte(c[1]), hi_byte(c[0]), hi_byte(cprev));
+        const uint32_t hi = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[fw] = hi;
+        w.KH[bw] = prmt(hi, (uint32_t)hi_byte(cprev), 0x4012);
     }
 }
 
@@ -683,17 +687,19 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
             const int awB = (P.xoff + ah - 4) >> 2;
             const uint32_t asB = sel4r((P.xoff + ah) & 3);
+            // C_b += mul x_{a+2t} + mul x_{a-2t} as two IDP4A with the one-hot int8 selector
+            // mul e_b (no byte unpacking)
+            const uint32_t mb = (uint32_t)mul & 0xffu;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
                 if (jj < nj && s < S) {
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
-                    int dc[4];
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        dc[b] = mul * (sbyte(fw, b) + sbyte(bw, b));
-                        C[jj][b] += dc[b];
+                        const int e = (int)(mb << (8 * b));
+                        C[jj][b] = __dp4a((int)fw, e, __dp4a((int)bw, e, C[jj][b]));
                         if (P.debug_check) esp += C[jj][b] * C[jj][b];
                     }
                     // bits above 7 of C + 128 set <=> |C| > 127 (wide kernel bytes needed)
