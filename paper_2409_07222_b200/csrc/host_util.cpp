@@ -196,7 +196,7 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.nwx = (wp.kp1 + 3) / 4;
     // X arrays: backward reads down to index -(4S+4) (C update), forward reads up to
     // k/2 + 4S + 8 (C update), 4*nwx (main loop) and 4*(nwx+S+2) (correlation init).
-    wp.xoff = 4 * wp.S + 8;
+    wp.xoff = 4 * round_up(wp.S + 2, 2);  // >= 4S+8, and the G loop's X words 8-byte aligned
     const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3)});
     wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
     // kernel: main loop reads d in [-(p+lpw R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4S+4

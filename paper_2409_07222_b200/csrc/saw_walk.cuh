@@ -89,11 +89,9 @@ __device__ __forceinline__ int sbyte(uint32_t w, int b) {  // one PRMT, sign-rep
 // acc[] accumulates onto its incoming value (the wide path runs the high-byte kernel
 // first, scales by 256 and continues with the low bytes in the same registers).
 template <int R>
-__device__ __forceinline__ void g_step(const uint32_t* __restrict__ Xw,
-                                       const uint32_t* __restrict__ Kw, int w, int j, int kb,
-                                       uint32_t sel, uint32_t (&KW)[R], uint32_t& rw,
+__device__ __forceinline__ void g_step(uint32_t x, const uint32_t* __restrict__ Kw, int w, int j,
+                                       int kb, uint32_t sel, uint32_t (&KW)[R], uint32_t& rw,
                                        int (&acc)[R]) {
-    const uint32_t x = Xw[w];
     const uint32_t nw = Kw[kb + w + 2];
 #pragma unroll
     for (int m = 0; m < R; ++m) acc[m] = __dp4a((int)x, (int)KW[(j - m + R) % R], acc[m]);
@@ -108,7 +106,7 @@ struct GTail {
                                                int kb, uint32_t sel, uint32_t (&KW)[R],
                                                uint32_t& rw, int (&acc)[R]) {
         if (J < rem) {
-            g_step<R>(Xw, Kw, w0 + J, J, kb, sel, KW, rw, acc);
+            g_step<R>(Xw[w0 + J], Kw, w0 + J, J, kb, sel, KW, rw, acc);
             GTail<R, J + 1>::run(Xw, Kw, w0, rem, kb, sel, KW, rw, acc);
         }
     }
@@ -130,8 +128,17 @@ __device__ __forceinline__ void g_neighbours(const uint32_t* __restrict__ Xw,
     uint32_t rw = Kw[kb + 1];
     const int nfull = (nwx / R) * R;
     for (int w0 = 0; w0 < nfull; w0 += R) {
+        if constexpr (R % 2 == 0) {  // X words in pairs (Xw is 8-byte aligned, w0 even)
 #pragma unroll
-        for (int j = 0; j < R; ++j) g_step<R>(Xw, Kw, w0 + j, j, kb, sel, KW, rw, acc);
+            for (int j = 0; j < R; j += 2) {
+                const uint2 xx = *reinterpret_cast<const uint2*>(Xw + w0 + j);
+                g_step<R>(xx.x, Kw, w0 + j, j, kb, sel, KW, rw, acc);
+                g_step<R>(xx.y, Kw, w0 + j + 1, j + 1, kb, sel, KW, rw, acc);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j) g_step<R>(Xw[w0 + j], Kw, w0 + j, j, kb, sel, KW, rw, acc);
+        }
     }
     // remainder steps j = 0 .. nwx - nfull - 1: nested guards, so a remainder of r costs
     // r + 1 tests instead of R
