@@ -54,3 +54,58 @@ def test_solve_matches_reference_pipeline(tmp_path, args, exe):
     assert got[1].split("fingerprint=")[1] == want[1].split("fingerprint=")[1]
     assert got[2] == want[2]                      # results file (deterministic: wall 0)
     assert got[3] == want[3]                      # candidate file, emission order
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exe", [SOLVE_S1, SOLVE_B200], ids=["gpu_step1", "gpu_step1_step2"])
+def test_experiment_matches_reference(tmp_path, exe):
+    # experiment_compare (pipeline.cpp:390-438) runs two Step-1 pools
+    # per run; with the B200 pool its per-run energies, medians and rank-sum test must be
+    # the reference's
+    if not os.access(SOLVE_REF, os.X_OK):
+        pytest.skip("reference solve not built")
+    args = ("experiment -L 61 --runs 5 --walkers 8 --restarts 3 --target-f 4.0 --tu 80 "
+            "--tr 3 --refine-top 3 --seed 5").split()
+    outs = []
+    for tag, e in (("b200", exe), ("ref", SOLVE_REF)):
+        csv = tmp_path / f"{tag}.csv"
+        r = subprocess.run([e, *args, "--out", str(csv)], capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr
+        outs.append((r.stdout, csv.read_text()))
+    assert outs[0] == outs[1]
+    assert outs[0][1].count("\n") == 6  # header + 5 runs
+
+
+@pytest.mark.gpu
+def test_verify_accepts_gpu_written_records(tmp_path):
+    # verify_records (pipeline.cpp:335-388) over the GPU Step-1 TSVs:
+    # the `labs saw` candidate file and the solve candidate/results files
+    labs_cli = os.path.join(ROOT, "paper_2409_07222_b200", "_lib", "labs")
+    saw = tmp_path / "saw.tsv"
+    r = subprocess.run([labs_cli, "saw", "-L", "101", "--walkers", "64", "--p", "8",
+                        "--restarts", "4", "--target-f", "4.5", "--out", str(saw)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    _, _, out, cands = _run(SOLVE_B200, "-L 45 --rounds 1 --walkers 8 --restarts 2 --target-f 4.0 "
+                            "--refine-top 3 --tu 90 --tr 3 --seed 3 --threads 1 --deterministic "
+                            "--no-construct".split(), tmp_path, "v")
+    files = [str(saw), str(tmp_path / "v_out.tsv"), str(tmp_path / "v_cands.tsv")]
+    r = subprocess.run([SOLVE_B200, "verify", *files], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout
+    lines = r.stdout.strip().splitlines()
+    assert len(lines) == 3 and all("0 mismatches, 0 malformed" in x for x in lines)
+    assert int(lines[0].split(": ")[1].split()[0]) == len(saw.read_text().splitlines()) > 0
+
+
+def test_verify_flags_corrupted_record(tmp_path):
+    # (CPU) the verify path itself: a record whose stored energy disagrees is reported,
+    # exit status 1 (labs_main.cpp:276-290)
+    bad = tmp_path / "bad.tsv"
+    # L=5 skew optimum +++-+ (hex 1D) has E=2; line 1 stores 3 instead
+    bad.write_text("5\t3\t4.1667\t1D\tsaw\n5\t2\t6.2500\t1D\tsaw\nnot a record\n")
+    r = subprocess.run([SOLVE_B200, "verify", str(bad)], capture_output=True, text=True,
+                       timeout=60)
+    assert r.returncode == 1
+    assert "2 records, 1 mismatches, 1 malformed" in r.stdout
+    assert "energy mismatch" in r.stdout
