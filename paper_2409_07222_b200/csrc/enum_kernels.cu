@@ -53,13 +53,6 @@ struct EnumLaunch {
 __device__ __forceinline__ uint32_t sel4(int o) { return 0x3210u + 0x1111u * (uint32_t)o; }
 // bytes o+3..o (reversed): (o+3) | (o+2)<<4 | (o+1)<<8 | o<<12
 __device__ __forceinline__ uint32_t sel4r(int o) { return 0x0123u + 0x1111u * (uint32_t)o; }
-__device__ __forceinline__ int sbyte(uint32_t w, int b) {  // one PRMT, sign-replicate mode
-    // (selector nibble 8|b copies the sign of byte b; __byte_perm drops that bit, so PTX)
-    uint32_t r;
-    const uint32_t sel = (uint32_t)(b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
-    return (int)r;
-}
 
 // One chunk of Gray codes per segment of LPW lanes (LPW = 16: two chunks per warp, the
 // per-step bookkeeping -- ctz, addresses, the flip stores, loop control -- serves both).
@@ -179,6 +172,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             const int tw = (tstar - 1) >> 2;
             const uint32_t tmask = ~(0xffu << (8 * ((tstar - 1) & 3)));
             int acc = 0;
+            const uint32_t mb = (uint32_t)mul & 0xffu;  // int8 mul: one-hot IDP4A selectors
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const int sw = sl + LPW * j;
@@ -189,7 +183,10 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
                     if (sw == tw) fw &= tmask;
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        const int dc = mul * (sbyte(fw, b) + sbyte(bw, b));  // 0 beyond k
+                        // dc = mul (x_{a+2t} + x_{a-2t}): two IDP4A against mul e_b, no
+                        // byte unpacking (0 beyond k)
+                        const int e = (int)(mb << (8 * b));
+                        const int dc = __dp4a((int)fw, e, __dp4a((int)bw, e, 0));
                         acc += dc * (2 * C[j][b] + dc);
                         C[j][b] += dc;
                     }
