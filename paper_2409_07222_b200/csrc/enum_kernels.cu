@@ -46,6 +46,7 @@ struct EnumLaunch {
     uint32_t* rec;                      // [rec_cap][4]: g lo, g hi, E, 0
     int64_t rec_cap;
     unsigned long long* rec_count;
+    unsigned long long* chunk_next;     // dynamic chunk-group queue (zeroed per launch)
     int64_t* chunk_best;                // [nchunks][2]: best E, its first g
 };
 
@@ -252,6 +253,22 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
 }
 
 template <int NJ, int LPW>
+__global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P);
+
+// Launch with one wave of resident blocks (the occupancy limit per SM x SMs), capped by
+// the work; the chunk queue balances the rest.
+template <int NJ, int LPW>
+void launch_enum(const EnumLaunch& P, size_t smem, cudaStream_t stream, int sms, uint64_t want) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, enum_kernel<NJ, LPW>, 128, smem) !=
+            cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(want, static_cast<uint64_t>(sms) * per_sm)));
+    enum_kernel<NJ, LPW><<<grid, 128, smem, stream>>>(P);
+}
+
+template <int NJ, int LPW>
 __global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P) {
     extern __shared__ uint32_t esmem[];
     constexpr int SEGS = 32 / LPW;
@@ -259,11 +276,16 @@ __global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumL
     const int seg = lane / LPW, sl = lane % LPW;
     int8_t* X0 = reinterpret_cast<int8_t*>(esmem + (warp * SEGS + seg) * P.warp_words);
     int8_t* X1 = X0 + 4 * P.xwords;
+    // chunk groups (SEGS chunks per warp) come from an atomic queue, so warps that finish
+    // early take more and no SM idles at the end of the launch
     const uint64_t ngrp = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t grp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; grp * SEGS < P.nchunks;
-         grp += ngrp) {
+    uint64_t grp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    while (grp * SEGS < P.nchunks) {
         const uint64_t c = grp * SEGS + seg;
         enum_chunk<NJ, LPW>(P, X0, X1, c < P.nchunks ? c : 0, c < P.nchunks, sl);
+        unsigned long long nx = 0;
+        if (lane == 0) nx = atomicAdd(P.chunk_next, 1ull);
+        grp = ngrp + __shfl_sync(FULLMASK, nx, 0);
     }
 }
 
@@ -366,7 +388,7 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
     float ms_total = 0;
     do {
         cudaError_t ce = cudaSuccess;
-        if (!cnt.p) ce = cudaMalloc(&cnt.p, sizeof(unsigned long long));
+        if (!cnt.p) ce = cudaMalloc(&cnt.p, 2 * sizeof(unsigned long long));  // count, queue
         if (ce == cudaSuccess && !best.p) ce = cudaMalloc(&best.p, 16 * P.nchunks);
         if (ce == cudaSuccess) {
             if (rec.p) cudaFree(rec.p);
@@ -381,8 +403,9 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         P.rec = rec.p;
         P.rec_cap = cap;
         P.rec_count = cnt.p;
+        P.chunk_next = cnt.p + 1;
         P.chunk_best = best.p;
-        cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), stream);
+        cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), stream);
         // 8 or 16 lanes per chunk (four or two chunks per warp) while a lane owns <= 4 lag
         // words; LABS_ENUM_LPW=8|16|32 forces a width (A/B timing)
         const char* lenv = std::getenv("LABS_ENUM_LPW");
@@ -394,29 +417,28 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const uint64_t want = (P.nchunks + 4 * segs - 1) / (4 * segs);
-        const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sms) * 8));
         const int nj = (P.S + lpw - 1) / lpw;
         cudaEventRecord(e0, stream);
         if (lpw == 8) {
             switch (nj) {
-                case 1: enum_kernel<1, 8><<<grid, 128, smem, stream>>>(P); break;
-                case 2: enum_kernel<2, 8><<<grid, 128, smem, stream>>>(P); break;
-                case 3: enum_kernel<3, 8><<<grid, 128, smem, stream>>>(P); break;
-                default: enum_kernel<4, 8><<<grid, 128, smem, stream>>>(P); break;
+                case 1: launch_enum<1, 8>(P, smem, stream, sms, want); break;
+                case 2: launch_enum<2, 8>(P, smem, stream, sms, want); break;
+                case 3: launch_enum<3, 8>(P, smem, stream, sms, want); break;
+                default: launch_enum<4, 8>(P, smem, stream, sms, want); break;
             }
         } else if (lpw == 16) {
             switch (nj) {
-                case 1: enum_kernel<1, 16><<<grid, 128, smem, stream>>>(P); break;
-                case 2: enum_kernel<2, 16><<<grid, 128, smem, stream>>>(P); break;
-                case 3: enum_kernel<3, 16><<<grid, 128, smem, stream>>>(P); break;
-                default: enum_kernel<4, 16><<<grid, 128, smem, stream>>>(P); break;
+                case 1: launch_enum<1, 16>(P, smem, stream, sms, want); break;
+                case 2: launch_enum<2, 16>(P, smem, stream, sms, want); break;
+                case 3: launch_enum<3, 16>(P, smem, stream, sms, want); break;
+                default: launch_enum<4, 16>(P, smem, stream, sms, want); break;
             }
         } else {
             switch (nj) {
-                case 1: enum_kernel<1, 32><<<grid, 128, smem, stream>>>(P); break;
-                case 2: enum_kernel<2, 32><<<grid, 128, smem, stream>>>(P); break;
-                case 3: enum_kernel<3, 32><<<grid, 128, smem, stream>>>(P); break;
-                default: enum_kernel<4, 32><<<grid, 128, smem, stream>>>(P); break;
+                case 1: launch_enum<1, 32>(P, smem, stream, sms, want); break;
+                case 2: launch_enum<2, 32>(P, smem, stream, sms, want); break;
+                case 3: launch_enum<3, 32>(P, smem, stream, sms, want); break;
+                default: launch_enum<4, 32>(P, smem, stream, sms, want); break;
             }
         }
         cudaEventRecord(e1, stream);
