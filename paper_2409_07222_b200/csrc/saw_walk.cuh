@@ -413,6 +413,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     // so that one IMAD, T' - xs' G, yields the key itself (wrapping mod 2^32 exactly like
     // the unsigned key).  Longer lengths keep the plain delta (sc = 1).
     const bool one_key = L <= 1001;
+    const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
     uint32_t T[R];  // (unsigned: the key form wraps mod 2^32; meaningless for a > k, masked)
     int xs[R];
@@ -697,6 +698,9 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             // C_b += mul x_{a+2t} + mul x_{a-2t} as two IDP4A with the one-hot int8 selector
             // mul e_b (no byte unpacking)
             const uint32_t mb = (uint32_t)mul & 0xffu;
+            int e1h[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) e1h[b] = (int)(mb << (8 * b));
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
@@ -704,11 +708,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int e = (int)(mb << (8 * b));
-                        C[jj][b] = __dp4a((int)fw, e, __dp4a((int)bw, e, C[jj][b]));
-                        if (P.debug_check) esp += C[jj][b] * C[jj][b];
-                    }
+                    for (int b = 0; b < 4; ++b)
+                        C[jj][b] = __dp4a((int)fw, e1h[b], __dp4a((int)bw, e1h[b], C[jj][b]));
                     // bits above 7 of C + 128 set <=> |C| > 127 (wide kernel bytes needed)
                     cmx |= ((C[jj][0] + 128) | (C[jj][1] + 128)) | ((C[jj][2] + 128) | (C[jj][3] + 128));
                 }
@@ -731,7 +732,12 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             if (sl == 1 && !cen) Xa[bstar >> 1] = (int8_t)(-xb);
             if (sl == 2) w.half[as >> 5] ^= 1u << (as & 31);
         }
-        if (P.debug_check) {
+        if (dbg) {  // (debug_check_energy: E re-derived from the C registers every step)
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj)
+                if (step && jj < nj && sl + LPW * jj < S)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) esp += C[jj][b] * C[jj][b];
             const int echk = sg.sum(esp);
             if (step && echk != energy) ++diverged;  // (energy already includes dstar)
         }
