@@ -793,11 +793,9 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 // instead of spilling.
 template <int R, int LPW>
 struct MinBlocks {
-#ifdef LABS_MINB_OLD
-    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 3 : 2) : (R <= 12 ? 3 : 2));
-#else
+    // (4 blocks = 128 registers: R <= 14 fits without spills since the wide pass shares
+    // the narrow pass's accumulators; 3 blocks = 168 registers for R = 15, 16)
     static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 3) : (R <= 16 ? 3 : 2));
-#endif
 };
 
 template <int R, int LPW, bool COUNT>
