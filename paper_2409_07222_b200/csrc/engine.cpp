@@ -330,7 +330,7 @@ std::vector<std::unique_ptr<DeviceRunner>>& g_runner_pool = *new std::vector<std
 bool same_geometry(const WalkParams& a, const WalkParams& b) {
     return a.L == b.L && a.p == b.p && a.t_i == b.t_i && a.bloom_bits == b.bloom_bits &&
            a.bloom_k == b.bloom_k && a.count_visited == b.count_visited &&
-           a.debug_check == b.debug_check;
+           a.debug_check == b.debug_check && a.lpw == b.lpw && a.R == b.R;  // (LABS_LPW)
 }
 
 std::unique_ptr<DeviceRunner> acquire_runner(int dev, const WalkParams& wp) {
