@@ -795,7 +795,8 @@ template <int R, int LPW>
 struct MinBlocks {
     // (4 blocks = 128 registers: R <= 14 fits without spills since the wide pass shares
     // the narrow pass's accumulators; 3 blocks = 168 registers for R = 15, 16)
-    static constexpr int value = R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 3) : (R <= 16 ? 3 : 2));
+    static constexpr int value =
+        R <= 6 ? 5 : (R <= 8 ? 4 : (LPW == 16 ? (R <= 14 ? 4 : 3) : (R <= 16 ? 3 : 2)));
 };
 
 template <int R, int LPW, bool COUNT>
