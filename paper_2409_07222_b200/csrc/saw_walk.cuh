@@ -416,7 +416,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
     uint32_t T[R];  // (unsigned: the key form wraps mod 2^32; meaningless for a > k, masked)
-    int xs[R];
+    int xs[R];  // NEGATED, key-scaled: -512 * 8 x_a (-512 * 4 x_k), so a key is one IMAD
     {
         const int16_t* C16h = reinterpret_cast<const int16_t*>(w.C16);
 #pragma unroll
@@ -432,7 +432,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                 xs[m] = 4 * (int)Xmine[a >> 1];
             }
             T[m] = (uint32_t)(t * sc) + (one_key ? kbase + 8u * m : 0u);
-            xs[m] *= sc;
+            xs[m] *= -sc;
         }
     }
 
@@ -505,7 +505,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         int delta[R];
 #pragma unroll
         for (int m = 0; m < R; ++m)  // the key if one_key
-            delta[m] = (int)(T[m] - (uint32_t)xs[m] * (uint32_t)acc[m]);
+            delta[m] = (int)(T[m] + (uint32_t)xs[m] * (uint32_t)acc[m]);
         if (score_out) {
             if (valid)
 #pragma unroll
@@ -684,7 +684,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                 if (3 * (a0 + 8 * m) == ex3) xp = 0;
                 const bool own = dstar_l == 8 * m;  // (x_{2a*-a*} = x_{a*} reads the zeroed 0)
                 T[m] += (uint32_t)(cmul * (f + g) + qa * xp + qb * (own ? 0 : g));
-                xs[m] = own ? -xs[m] : xs[m];
+                const int om = own ? -1 : 0;  // (negation on the ALU: (x ^ -1) + 1)
+                xs[m] = (xs[m] ^ om) - om;
             }
         }
         // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
@@ -700,7 +701,8 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const uint32_t mb = (uint32_t)mul & 0xffu;
             int e1h[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) e1h[b] = (int)(mb << (8 * b));
+            for (int b = 0; b < 4; ++b)  // mul in byte b, zeros elsewhere (PRMT, not a shift)
+                e1h[b] = (int)prmt(mb, 0u, 0x4444u ^ (0x4u << (4 * b)));
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
