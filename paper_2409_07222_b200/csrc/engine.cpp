@@ -257,6 +257,9 @@ public:
     // Enqueue K1 and the drains of the record count and the per-walk stats on this
     // runner's stream, without waiting (the pipelined pool overlaps the host replay of
     // the previous batch with it).
+    // halves_at: the packed halves of these walks when they live elsewhere (the pipelined
+    // pool seeds every batch at once into one runner's buffer); default: this runner's
+    const uint32_t* halves_at = nullptr;
     void walk_launch(int64_t nwalks, int* score_out = nullptr, int* corr_out = nullptr) {
         stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
         if (rec_cap == 0) {
@@ -265,7 +268,7 @@ public:
         }
         WalkParams P = wp;
         P.nwalks = nwalks;
-        P.halves = halves.p;
+        P.halves = halves_at ? halves_at : halves.p;
         P.rec = rec.p;
         P.rec_cap = rec_cap;
         P.rec_count = rec_count.p;
@@ -733,8 +736,33 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                     kMaxBatchWalks, nb == 1 ? total : std::max<int64_t>(2 * resident, (total + nb - 1) / nb));
                 const auto batches = make_batches(walkers, chunk);
                 std::vector<BatchOut> bo(batches.size());
-                std::vector<int64_t> nws(batches.size());
-                Carry carry;
+                std::vector<int64_t> nws(batches.size()), off(batches.size());
+                // K3 once for the whole pool (walker order = batch order), so no batch waits on
+                // a seed launch queued behind the other stream's walk kernel
+                {
+                    std::vector<Segment> all;
+                    for (uint32_t w : walkers) all.push_back(Segment{w, 0, R});
+                    std::vector<std::array<uint64_t, 4>> states(all.size());
+                    std::vector<int32_t> init(all.size(), 1);
+                    BatchOut sb;
+                    slot[0]->seed(all, d, cfg.seed, states, init, total, sb);
+                    acc.st.seed_ms += sb.seed_ms;
+                    acc.st.h2d_bytes += sb.h2d;
+                    acc.st.d2h_bytes += sb.d2h;
+                }
+                int64_t o = 0;
+                for (size_t i = 0; i < batches.size(); ++i) {
+                    off[i] = o;
+                    nws[i] = 0;
+                    for (const Segment& sg : batches[i]) {
+                        for (int64_t r = sg.r0; r < sg.r1; ++r) {
+                            bo[i].walk_walker.push_back(sg.walker);
+                            bo[i].walk_restart.push_back(r);
+                        }
+                        nws[i] += sg.r1 - sg.r0;
+                    }
+                    o += nws[i];
+                }
                 const auto tD = std::chrono::steady_clock::now();
                 double replay_ms = 0;
                 const auto retire = [&](size_t j) {  // wait for batch j, replay it, free it
@@ -753,11 +781,12 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
                 for (size_t i = 0; i < batches.size(); ++i) {
                     if (i >= 2) retire(retired++);  // batch i - 2: frees slot i % 2
                     if (sink.aborted || acc.diverged) break;
-                    nws[i] = seed_batch(*slot[i % 2], batches[i], carry, bo[i]);
+                    slot[i % 2]->halves_at = slot[0]->halves.p + static_cast<size_t>(off[i]) * wp.hw;
                     slot[i % 2]->walk_launch(nws[i]);
                     launched = i + 1;
                 }
                 while (retired < launched) retire(retired++);
+                slot[0]->halves_at = slot[1]->halves_at = nullptr;
                 if (std::getenv("LABS_TIMING"))
                     std::fprintf(stderr, "[labs] %zu pipelined batches of <= %lld walks: %.2f ms, "
                                  "host replay %.2f ms (overlapped)\n", batches.size(),
