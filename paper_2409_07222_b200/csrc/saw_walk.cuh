@@ -1,7 +1,8 @@
 // saw_walk.cuh -- K1, the sm_100a walk kernel of Step 1 of the dual-step LABS search
 // (templates; instantiated per (R, LPW) in saw_walk_r*.cu, launched from saw_kernels.cu).
 //
-// K1 saw_walk_kernel : 32 or 16 lanes = one self-avoiding walk (run_walk, saw.cpp:117-149).
+// K1 saw_walk_kernel : 8, 16 or 32 lanes = one self-avoiding walk (run_walk, saw.cpp:117-149);
+//                      warps take groups of walks from an atomic queue.
 //                      Fuses the Bloom probe, the skew flip-delta of every free
 //                      neighbour (skew_flip_delta_fast, skew.cpp:60-93), the
 //                      lexicographic argmin (best_neighbour, saw.cpp:106-115), the
@@ -321,9 +322,10 @@ struct LagWords {  // lag words a lane may own: s = sl + LPW jj, S = ceil(k/4) <
 // K1: LPW lanes = one walk.  The per-neighbour constant part of the delta
 //     T(a) = 16 N(a) + 32 Q(a) + 8 (-1)^(k-a) C_{2(k-a)}   (a < k),   4 N + 8 Q  (a = k)
 // and xs(a) = 8 x_a (4 x_k) live in the owning lane's registers, so a delta is one IMAD on
-// the sliding dot product G(a): dE(a) = T(a) - xs(a) G(a).  Per step T is updated in O(1)
-// per neighbour (Q pairs through the flipped positions, and the C term from the per-lag
-// dc bytes the C update publishes); the exact even-lag C live in the lag owners' registers.
+// the sliding dot product G(a): dE(a) = T(a) - xs(a) G(a) (for L <= 1001 both are kept
+// key-scaled, so that IMAD yields the argmin key itself).  Per step T is updated in O(1) per
+// neighbour (the C term and the Q pairs through the flipped positions, read from the zeroed
+// pre-step sequence); the exact even-lag C live in the lag owners' registers.
 template <int R, int LPW, bool COUNT>
 __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint64_t* fm0,
                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
