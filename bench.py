@@ -126,22 +126,42 @@ def cpu_sample(walkers_hint=None):
     return cores, n
 
 
-def reference_cpu(threads, walkers, reps=1, warmup=0):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _sample_config(walkers):
+    from oracle.oracle import make_config
+    return make_config(L, walkers=WALKERS_PER_GPU, prefix_len=P, target_merit=F, max_restarts=1,
+                       seed=SEED, walker_end=walkers)
+
+
+def reference_cpu(threads, walkers, reps=1, warmup=0, trace=True):
     """The reference's CPU path on the host: oracle/_ref (the reference library compiled from
-    its own sources) when present, else the C restatement.  Returns (kind, [seconds], stats,
-    delta_evals).  The delta count comes from the reference's own run_walk through its
-    VisitedSet seam (untimed)."""
-    from oracle.oracle import Reference, Restated, make_config, reference_available
-    cfg = make_config(L, walkers=walkers, prefix_len=P, target_merit=F, max_restarts=1, seed=SEED)
+    its own sources) when present, else the C restatement.  Timed: the stock run_saw_pool
+    (saw.cpp:218-267) with `threads` std::threads on walkers [0, walkers) x 1 restart of C4.
+    Untimed (trace=True): the same walks through the reference's run_walk with a counting
+    VisitedSet, replayed in --threads 1 order through its DedupSink -- the delta-eval count
+    and the ordered candidate list the GPU parity diff uses."""
+    from oracle.oracle import Reference, Restated, reference_available
+    cfg = _sample_config(walkers)
+    tr = None
     if reference_available():
         lib, kind = Reference(), "reference"
-        evals = lib.count_deltas(cfg, threads)["delta_evals"]
+        if trace:
+            tr = lib.walk_trace_mt(cfg, threads)
         run = lambda: lib.run_saw_pool(cfg, threads=threads)  # noqa: E731
     else:
         lib, kind = Restated(), "port"
         threads = 1
         run = lambda: lib.run_saw_pool(cfg)  # noqa: E731
-        evals = None
     times, res = [], None
     for i in range(warmup + reps):
         t0 = time.perf_counter()
@@ -149,18 +169,66 @@ def reference_cpu(threads, walkers, reps=1, warmup=0):
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    if evals is None:
-        evals = res.stats["delta_evals"]
-    return kind, times, res.stats, evals, threads
+    if tr is None:
+        tr = res if kind == "port" else None
+    evals = tr.stats["delta_evals"] if tr is not None else None
+    return dict(kind=kind, times=times, stats=res.stats, evals=evals, threads=threads, trace=tr)
+
+
+def single_thread_leg(walkers=None):
+    """threads = 1 rate of the reference: a smaller sample, timed."""
+    from oracle.oracle import Reference, reference_available
+    if not reference_available():
+        return None
+    n = walkers or int(os.environ.get("BENCH_CPU_WALKERS_1T", "0")) or 16
+    lib = Reference()
+    cfg = _sample_config(n)
+    evals = lib.count_deltas(cfg, os.cpu_count() or 1)["delta_evals"]
+    t0 = time.perf_counter()
+    lib.run_saw_pool(cfg, threads=1)
+    dt = time.perf_counter() - t0
+    return {"value": evals / dt, "unit": "flip-deltas/s", "cores": 1,
+            "sample": f"C4 walkers [0,{n}) x 1 restart, {evals} delta evals in {dt:.2f} s "
+                      f"(reference run_saw_pool, threads=1)"}
+
+
+def tsv_lines(cands, fmt):
+    """Candidate records with their (walker, restart) origin, in delivery order."""
+    return [f"{c.walker}\t{c.restart}\t{fmt(c.seq, c.energy)}" for c in cands]
+
+
+def gpu_parity(labs, ref, walkers):
+    """Headline-scale parity: the C4 walks the CPU leg ran -- walkers
+    [0, walkers) x 1 restart -- through the GPU's public run_saw_pool, diffed against the
+    reference's --threads 1 candidate list (same order, same records) and pool stats."""
+    import hashlib
+    cfg = labs.SawConfig(length=L, walkers=WALKERS_PER_GPU, prefix_len=P, target_merit=F,
+                         max_restarts=1, seed=SEED, walker_end=walkers, count_visited=True)
+    sink = labs.CollectingSink()
+    st = labs.run_saw_pool(cfg, sink)
+    got = tsv_lines(sink.take(), labs.format_record)
+    want = tsv_lines(ref.candidates, labs.format_record)
+    sha = lambda lines: hashlib.sha256("\n".join(lines).encode()).hexdigest()  # noqa: E731
+    stats = {k: (getattr(st, k), ref.stats[k])
+             for k in ("walks", "iterations", "emitted", "best_energy", "delta_evals")}
+    same_stats = all(a == b for a, b in stats.values())
+    return {"workload": f"C4 walkers [0,{walkers}) x 1 restart (L={L} p={P} F>={F} seed={SEED})",
+            "walks": st.walks, "candidates_gpu": len(got), "candidates_reference": len(want),
+            "sha256_gpu": sha(got), "sha256_reference": sha(want),
+            "stats_gpu_vs_reference": stats,
+            "identical": got == want and same_stats,
+            "compared": "ordered TSV records (walker, restart, L, E, F, hex, origin) and pool "
+                        "stats (walks, iterations, emitted, best E, delta evals); reference = "
+                        "its run_walk + DedupSink in --threads 1 order (oracle/_ref)"}
 
 
 def run_reference_arm(args, ws, rank):
     if rank != 0:
         return
     threads, walkers = cpu_sample()
-    kind, times, stats, evals, threads = reference_cpu(threads, walkers, args.steps, args.warmup)
-    t = statistics.mean(times)
-    v = evals / t
+    r = reference_cpu(threads, walkers, args.steps, args.warmup)
+    t = statistics.mean(r["times"])
+    v = r["evals"] / t
     line = {
         "impl": "reference", "metric": "flip-delta evals/sec (L=451)", "value": v,
         "unit": "flip-deltas/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -168,11 +236,12 @@ def run_reference_arm(args, ws, rank):
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"C4 sample: L={L} p={P} F>={F} T_i=1808 fpr=1e-4 seed=1, "
                                f"walkers [0,{walkers}) x 1 restart",
-                   "threads": threads},
-        "candidates_per_s": stats["emitted"] / t,
-        "cpu_baseline": {"value": v, "unit": "flip-deltas/s", "cores": threads, "kind": kind,
-                         "sample": f"C4 walkers [0,{walkers}) x 1 restart ({evals} delta evals "
-                                   f"per step, run_saw_pool threads={threads})"},
+                   "threads": r["threads"]},
+        "candidates_per_s": r["stats"]["emitted"] / t,
+        "cpu_baseline": {"value": v, "unit": "flip-deltas/s", "cores": r["threads"],
+                         "kind": r["kind"], "cpu_model": cpu_model(),
+                         "sample": f"C4 walkers [0,{walkers}) x 1 restart ({r['evals']} delta "
+                                   f"evals per step, run_saw_pool threads={r['threads']})"},
         "e2e": {"value": v, "unit": "flip-deltas/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -290,18 +359,21 @@ def main():
                             f"delta = inner product of (L+1)/2 = {(L + 1) // 2} int8 MACs",
                 "kernel_ms_per_launch": st.kernel_ms,
                 "ref_equiv_tops": deltas_all * REF_OPS_PER_DELTA / step_s / 1e12}
-        cpu = None
+        cpu, parity = None, None
         if not args.no_cpu_baseline:
             try:
                 threads, cw = cpu_sample()
-                kind, times, cst2, evals, threads = reference_cpu(threads, cw)
-                dt = times[0]
-                cpu = {"value": evals / dt, "unit": "flip-deltas/s", "cores": threads,
-                       "kind": kind, "sample": f"C4 walkers [0,{cw}) x 1 restart, "
-                                               f"{evals} delta evals in {dt:.2f} s "
-                                               f"(reference run_saw_pool, {threads} threads)"}
+                r = reference_cpu(threads, cw)
+                dt = r["times"][0]
+                cpu = {"value": r["evals"] / dt, "unit": "flip-deltas/s", "cores": r["threads"],
+                       "kind": r["kind"], "cpu_model": cpu_model(),
+                       "sample": f"C4 walkers [0,{cw}) x 1 restart, {r['evals']} delta evals "
+                                 f"in {dt:.2f} s (reference run_saw_pool, {r['threads']} threads)",
+                       "threads_1": single_thread_leg()}
+                if r["trace"] is not None:
+                    parity = gpu_parity(labs, r["trace"], cw)
             except Exception as e:  # baseline is reported, never fatal
-                cpu = {"value": None, "error": str(e)}
+                cpu = {"value": None, "error": f"{type(e).__name__}: {e}"}
         free = (L + 1) // 2 - P
         line = {
             "metric": "flip-delta evals/sec (L=451)",
@@ -333,6 +405,7 @@ def main():
             "gpu_launches": 2 * args.steps * ws,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": deltas_all / e2e_s, "unit": "flip-deltas/s",
                     "h2d_bytes_per_step": e2e_stats.h2d_bytes,
                     "d2h_bytes_per_step": e2e_stats.d2h_bytes,

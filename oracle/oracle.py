@@ -295,6 +295,8 @@ class Reference(_Base):
         L.ref_run_saw_pool.argtypes = [C.POINTER(SawConfigC), C.c_int, CAND_FN, C.c_void_p,
                                        C.POINTER(PoolStatsC)]
         L.ref_count_deltas.argtypes = [C.POINTER(SawConfigC), C.c_int, C.POINTER(PoolStatsC)]
+        L.ref_walk_trace_mt.argtypes = [C.POINTER(SawConfigC), C.c_int, CAND_FN, WALK_FN,
+                                        C.c_void_p, C.POINTER(PoolStatsC)]
         L.ref_walk_trace.argtypes = [C.POINTER(SawConfigC), CAND_FN, WALK_FN, C.c_void_p,
                                      C.POINTER(PoolStatsC)]
         for name in ("ref_skew_flip_delta_fast", "ref_skew_flip_delta"):
@@ -335,6 +337,17 @@ class Reference(_Base):
         run, cb, wb = self._collect()
         st = PoolStatsC()
         rc = self.lib.ref_walk_trace(C.byref(cfg), cb, wb, None, C.byref(st))
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        run.stats = _stats(st)
+        return run
+
+    def walk_trace_mt(self, cfg: SawConfigC, threads: int = 1) -> OracleRun:
+        """The reference run_walk over every (walker, restart), walkers on `threads` threads,
+        replayed in --threads 1 order through the reference DedupSink (ref_shim.cpp)."""
+        run, cb, wb = self._collect()
+        st = PoolStatsC()
+        rc = self.lib.ref_walk_trace_mt(C.byref(cfg), threads, cb, wb, None, C.byref(st))
         if rc != 0:
             raise ValueError(self.lib.ref_last_error().decode())
         run.stats = _stats(st)

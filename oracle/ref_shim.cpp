@@ -8,6 +8,8 @@
 #include <cstring>
 #include <atomic>
 #include <memory>
+#include <mutex>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -149,6 +151,104 @@ int ref_walk_trace(const lo_saw_config* cfg, lo_candidate_fn cand, lo_walk_fn wa
                 }
             }
         }
+        if (out) *out = st;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Threaded replica of ref_walk_trace: the reference's own run_walk for every (walker,
+// restart) of [walker_begin, walker_end), walkers spread over `threads` std::threads (a
+// walker's restarts stay on one thread, in order, on its own Rng stream and Bloom filter:
+// walker_loop, saw.cpp:196-214).  Each walk's raw emissions are kept, then replayed in
+// (walker, restart, emission) order through the reference DedupSink, so the candidate list
+// is the --threads 1 list of run_saw_pool (walks are independent without quota / time /
+// stop); per-walk stats carry the delta-eval counts.  Used by bench.py
+// for the headline-scale parity diff.
+int ref_walk_trace_mt(const lo_saw_config* cfg, int threads, lo_candidate_fn cand,
+                      lo_walk_fn walkcb, void* user, lo_pool_stats* out) {
+    try {
+        SawConfig sc = to_saw(cfg, 1);
+        sc.validate();
+        if (sc.max_restarts <= 0 || sc.time_budget_s > 0 || sc.candidate_quota > 0 ||
+            sc.stop_at_energy > 0)
+            throw std::invalid_argument("walk_trace_mt: needs independent walks");
+        const int p = sc.effective_prefix_len();
+        std::vector<PartitionPrefix> prefixes;
+        if (p == 0) prefixes.push_back(PartitionPrefix{{}, 0});
+        else prefixes = rank_prefixes(p);
+        const int w0 = cfg->walker_begin > 0 ? cfg->walker_begin : 0;
+        const int w1 = cfg->walker_end > 0 && cfg->walker_end < sc.walkers ? cfg->walker_end
+                                                                            : sc.walkers;
+        struct Walk {
+            std::vector<Candidate> cands;
+            WalkStats ws;
+            long long misses = 0;
+        };
+        const long long R = sc.max_restarts;
+        const int nw = std::max(0, w1 - w0);
+        std::vector<Walk> walks(static_cast<std::size_t>(nw) * static_cast<std::size_t>(R));
+        std::atomic<int> next{0};
+        auto job = [&]() {
+            class Keep final : public CandidateSink {
+            public:
+                std::vector<Candidate>* out = nullptr;
+                void emit(const Candidate& c) override { out->push_back(c); }
+            } keep;
+            for (int i = next++; i < nw; i = next++) {
+                const int w = w0 + i;
+                const std::size_t cls = static_cast<std::size_t>(w) % prefixes.size();
+                Rng rng(sc.seed, static_cast<std::uint64_t>(w));
+                CountingVisited visited(static_cast<std::size_t>(sc.effective_iterations()) + 1,
+                                        sc.bloom_fpr);
+                for (long long r = 0; r < R; ++r) {
+                    Walk& wk = walks[static_cast<std::size_t>(i) * R + r];
+                    keep.out = &wk.cands;
+                    const long long m0 = visited.misses;
+                    wk.ws = run_walk(sc, prefixes[cls], rng, visited, keep);
+                    wk.misses = visited.misses - m0;
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 0; t < (threads > 0 ? threads : 1); ++t) th.emplace_back(job);
+        for (auto& t : th) t.join();
+        CallbackSink user_sink(cand, user);
+        class Count final : public CandidateSink {
+        public:
+            explicit Count(CandidateSink& in) : inner(in) {}
+            void emit(const Candidate& c) override {
+                ++n;
+                inner.emit(c);
+            }
+            CandidateSink& inner;
+            long long n = 0;
+        } counted(user_sink);
+        DedupSink dedup(counted);
+        lo_pool_stats st;
+        std::memset(&st, 0, sizeof st);
+        bool best_set = false;
+        for (int i = 0; i < nw; ++i)
+            for (long long r = 0; r < R; ++r) {
+                const Walk& wk = walks[static_cast<std::size_t>(i) * R + r];
+                user_sink.walker = w0 + i;
+                user_sink.restart = r;
+                for (const Candidate& c : wk.cands) dedup.emit(c);
+                ++st.walks;
+                st.iterations += wk.ws.iterations;
+                st.delta_evals += wk.misses;
+                st.exhausted_walks += wk.ws.neighbourhood_exhausted ? 1 : 0;
+                if (walkcb)
+                    walkcb(user, w0 + i, r, wk.ws.iterations, wk.ws.emitted, wk.ws.best_energy,
+                           wk.misses, wk.ws.neighbourhood_exhausted ? 1 : 0, 0);
+                if (!best_set || wk.ws.best_energy < st.best_energy) {
+                    st.best_energy = wk.ws.best_energy;
+                    best_set = true;
+                }
+            }
+        st.emitted = counted.n;
         if (out) *out = st;
         return 0;
     } catch (const std::exception& e) {
