@@ -138,9 +138,11 @@ def cpu_model():
 
 
 def _sample_config(walkers):
+    """Walkers [0, walkers) x 1 restart of C4: walker w keeps its class (w mod 128) and its
+    Rng stream w, so these are exactly the first walks of the C4 pool."""
     from oracle.oracle import make_config
-    return make_config(L, walkers=WALKERS_PER_GPU, prefix_len=P, target_merit=F, max_restarts=1,
-                       seed=SEED, walker_end=walkers)
+    return make_config(L, walkers=walkers, prefix_len=P, target_merit=F, max_restarts=1,
+                       seed=SEED)
 
 
 def reference_cpu(threads, walkers, reps=1, warmup=0, trace=True):
@@ -202,8 +204,8 @@ def gpu_parity(labs, ref, walkers):
     [0, walkers) x 1 restart -- through the GPU's public run_saw_pool, diffed against the
     reference's --threads 1 candidate list (same order, same records) and pool stats."""
     import hashlib
-    cfg = labs.SawConfig(length=L, walkers=WALKERS_PER_GPU, prefix_len=P, target_merit=F,
-                         max_restarts=1, seed=SEED, walker_end=walkers, count_visited=True)
+    cfg = labs.SawConfig(length=L, walkers=walkers, prefix_len=P, target_merit=F,
+                         max_restarts=1, seed=SEED, count_visited=True)
     sink = labs.CollectingSink()
     st = labs.run_saw_pool(cfg, sink)
     got = tsv_lines(sink.take(), labs.format_record)

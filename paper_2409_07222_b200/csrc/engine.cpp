@@ -1,17 +1,18 @@
 // engine.cpp -- host orchestration of the Step-1 GPU path and the C ABI
-// (include/labs_gpu.h).  Replaces run_saw_pool (saw.cpp:218-267): walks are
-// enumerated in the reference's --threads 1 order (walker, restart), generated
-// and run on the GPU in batches, and their sieve hits are replayed on the host
-// through DedupSink -> CountingSink semantics (candidate.hpp:84-99,
-// saw.cpp:173-194) before reaching the caller's sink.
+// (include/labs_gpu.h).  Replaces run_saw_pool (saw.cpp:218-267): the pool's walks are
+// planned in the reference's order, cut into jobs that the per-device executors
+// (runner.hpp) seed, walk and compact on the GPU, and the finished jobs are replayed on the
+// host -- walk by walk, in the pool's order -- through DedupSink -> CountingSink semantics
+// (candidate.hpp:84-99, saw.cpp:173-194) before reaching the caller's sink.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <array>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -21,309 +22,16 @@
 #include <vector>
 
 #include "host_util.hpp"
+#include "runner.hpp"
 
 namespace labs_b200 {
-
-cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int* score_out,
-                            int* corr_out);
-cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st);
-int walk_blocks_per_sm(WalkParams& P);  // (also places the fm table)
 
 namespace {
 thread_local std::string g_error;
 }
 void set_error(const std::string& msg) { g_error = msg; }
 
-#define LABS_CUDA(call)                                                                    \
-    do {                                                                                   \
-        cudaError_t _e = (call);                                                           \
-        if (_e != cudaSuccess) {                                                           \
-            throw CudaFailure(std::string(#call) + ": " + cudaGetErrorString(_e));         \
-        }                                                                                  \
-    } while (0)
-
-struct CudaFailure : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-template <typename T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    void reserve(size_t count) {
-        if (count <= n) return;
-        release();
-        LABS_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
-        n = count;
-    }
-};
-
-// Grow-only pinned host staging (async D2H drains of the record buffer and walk stats).
-template <typename T>
-struct PinnedBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    PinnedBuf() = default;
-    PinnedBuf(const PinnedBuf&) = delete;
-    PinnedBuf& operator=(const PinnedBuf&) = delete;
-    ~PinnedBuf() {
-        if (p) cudaFreeHost(p);
-    }
-    void reserve(size_t count) {
-        if (count <= n) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        n = 0;
-        LABS_CUDA(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
-        n = count;
-    }
-};
-
-// One restart range of one walker, in --threads 1 order.
-struct Segment {
-    uint32_t walker;
-    int64_t r0, r1;
-};
-
-struct WalkRecordView {
-    int64_t walk;        // batch-local walk index
-    int64_t iteration;
-    int64_t energy;
-    uint64_t hash;       // canonical_hash(0) of the full sequence (computed on the device)
-    const uint32_t* half;
-};
-
-struct BatchOut {
-    std::vector<uint32_t> rec;    // count x rec_words
-    int64_t nrec = 0;
-    std::vector<int64_t> stats;   // nwalks x kWalkStatWords
-    std::vector<int64_t> walk_walker, walk_restart;  // per batch walk
-    double kernel_ms = 0, seed_ms = 0;
-    int64_t h2d = 0, d2h = 0;  // bytes copied for this batch
-};
-
-// Per-device state: stream, events, uploaded tables, batch buffers.
-class DeviceRunner {
-public:
-    int dev = 0;
-    cudaStream_t st = nullptr;
-    cudaEvent_t ev[4] = {};
-    WalkParams wp{};
-    int grid_cap = 0;
-    DevBuf<uint64_t> fm, tab, tabfull, rng;
-    DevBuf<uint32_t> halves, rec, seg_walker, seg_prefix;
-    DevBuf<int64_t> stats, seg_rest, seg_off;
-    DevBuf<int32_t> seg_init;
-    DevBuf<unsigned long long> rec_count;
-    PinnedBuf<uint32_t> h_rec;
-    PinnedBuf<int64_t> h_stats;
-    PinnedBuf<unsigned long long> h_count;
-    int64_t rec_cap = 0;
-
-    ~DeviceRunner() {
-        if (st) {
-            cudaSetDevice(dev);
-            for (auto& e : ev)
-                if (e) cudaEventDestroy(e);
-            cudaStreamDestroy(st);
-        }
-    }
-
-    void init(int device, const WalkParams& params) {
-        dev = device;
-        wp = params;
-        LABS_CUDA(cudaSetDevice(dev));
-        LABS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        for (auto& e : ev) LABS_CUDA(cudaEventCreate(&e));
-        const auto& tt = TabTables::get();
-        const int kp1 = wp.kp1, L = wp.L;
-        std::vector<uint64_t> hfm(3 * static_cast<size_t>(kp1));
-        std::vector<uint64_t> htab(4 * static_cast<size_t>(kp1));
-        std::vector<uint64_t> hfull(2 * static_cast<size_t>(L));
-        for (int t = 0; t < 2; ++t)
-            for (int i = 0; i < kp1; ++i) {
-                hfm[static_cast<size_t>(t) * kp1 + i] = tt.t[t][i][0] ^ tt.t[t][i][1];
-                htab[(static_cast<size_t>(t) * kp1 + i) * 2 + 0] = tt.t[t][i][0];
-                htab[(static_cast<size_t>(t) * kp1 + i) * 2 + 1] = tt.t[t][i][1];
-            }
-        for (int j = 0; j < L; ++j) {
-            hfull[2 * static_cast<size_t>(j)] = tt.t[0][j][0];
-            hfull[2 * static_cast<size_t>(j) + 1] = tt.t[0][j][1];
-        }
-        for (int j = 0; j < kp1; ++j) {  // a skew flip at half index j toggles j and L-1-j
-            uint64_t m = tt.t[0][j][0] ^ tt.t[0][j][1];
-            if (L - 1 - j != j) m ^= tt.t[0][L - 1 - j][0] ^ tt.t[0][L - 1 - j][1];
-            hfm[2 * static_cast<size_t>(kp1) + j] = m;
-        }
-        fm.reserve(hfm.size());
-        tab.reserve(htab.size());
-        tabfull.reserve(hfull.size());
-        LABS_CUDA(cudaMemcpyAsync(fm.p, hfm.data(), hfm.size() * 8, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(tab.p, htab.data(), htab.size() * 8, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(tabfull.p, hfull.data(), hfull.size() * 8, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaStreamSynchronize(st));  // host staging vectors die at scope end
-        wp.fm = fm.p;
-        wp.tab = tab.p;
-        wp.tabfull = tabfull.p;
-        wp.salt0 = tt.salt[0][kp1];
-        wp.salt1 = tt.salt[1][kp1];
-        wp.salt_full = tt.salt[0][L];
-        int sms = 0;
-        LABS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const int bps = std::max(1, walk_blocks_per_sm(wp));
-        grid_cap = sms * bps;
-        rec_count.reserve(2);  // [0] records emitted, [1] the kernel's walk-group queue
-    }
-
-    // Generate halves for the segments on the device (K3).
-    void seed(const std::vector<Segment>& segs, const Derived& d, uint64_t seed,
-              std::vector<std::array<uint64_t, 4>>& states, const std::vector<int32_t>& init,
-              int64_t nwalks, BatchOut& out) {
-        const int nseg = static_cast<int>(segs.size());
-        std::vector<uint32_t> hw(nseg), hp(nseg);
-        std::vector<int64_t> hr(nseg), ho(nseg);
-        std::vector<uint64_t> hs(4 * static_cast<size_t>(nseg));
-        int64_t off = 0;
-        for (int i = 0; i < nseg; ++i) {
-            hw[i] = segs[i].walker;
-            hp[i] = d.prefix_bits[segs[i].walker % static_cast<uint32_t>(d.nprefix)];
-            hr[i] = segs[i].r1 - segs[i].r0;
-            ho[i] = off;
-            off += hr[i];
-            for (int j = 0; j < 4; ++j) hs[4 * static_cast<size_t>(i) + j] = states[i][j];
-        }
-        seg_walker.reserve(nseg);
-        seg_prefix.reserve(nseg);
-        seg_rest.reserve(nseg);
-        seg_off.reserve(nseg);
-        seg_init.reserve(nseg);
-        rng.reserve(4 * static_cast<size_t>(nseg));
-        halves.reserve(static_cast<size_t>(nwalks) * wp.hw);
-        LABS_CUDA(cudaMemcpyAsync(seg_walker.p, hw.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(seg_prefix.p, hp.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(seg_rest.p, hr.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(seg_off.p, ho.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(seg_init.p, init.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-        LABS_CUDA(cudaMemcpyAsync(rng.p, hs.data(), 32 * static_cast<size_t>(nseg),
-                                  cudaMemcpyHostToDevice, st));
-        out.h2d += static_cast<int64_t>(nseg) * (4 + 4 + 8 + 8 + 4 + 32);
-        SeedParams sp{};
-        sp.kp1 = wp.kp1;
-        sp.p = wp.p;
-        sp.hw = wp.hw;
-        sp.nseg = nseg;
-        sp.seed = seed;
-        sp.walker_ids = seg_walker.p;
-        sp.prefix_bits = seg_prefix.p;
-        sp.seg_restarts = seg_rest.p;
-        sp.seg_offset = seg_off.p;
-        sp.seg_init = seg_init.p;
-        sp.rng_state = rng.p;
-        sp.halves = halves.p;
-        LABS_CUDA(cudaEventRecord(ev[2], st));
-        LABS_CUDA(launch_saw_seed(sp, st));
-        LABS_CUDA(cudaEventRecord(ev[3], st));
-        LABS_CUDA(cudaMemcpyAsync(hs.data(), rng.p, 32 * static_cast<size_t>(nseg),
-                                  cudaMemcpyDeviceToHost, st));
-        LABS_CUDA(cudaStreamSynchronize(st));
-        out.d2h += 32 * static_cast<int64_t>(nseg);
-        float ms = 0;
-        LABS_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
-        out.seed_ms += ms;
-        for (int i = 0; i < nseg; ++i)
-            for (int j = 0; j < 4; ++j) states[i][j] = hs[4 * static_cast<size_t>(i) + j];
-    }
-
-    void upload_halves(const std::vector<uint32_t>& h, int64_t nwalks) {
-        halves.reserve(static_cast<size_t>(nwalks) * wp.hw);
-        LABS_CUDA(cudaMemcpyAsync(halves.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
-    }
-
-    // Run K1 over `nwalks` walks whose halves are resident; copy back records + stats.
-    void walk(int64_t nwalks, BatchOut& out, int* score_out = nullptr, int* corr_out = nullptr) {
-        walk_launch(nwalks, score_out, corr_out);
-        walk_finish(nwalks, out, score_out, corr_out);
-    }
-
-    // Enqueue K1 and the drains of the record count and the per-walk stats on this
-    // runner's stream, without waiting (the pipelined pool overlaps the host replay of
-    // the previous batch with it).
-    // halves_at: the packed halves of these walks when they live elsewhere (the pipelined
-    // pool seeds every batch at once into one runner's buffer); default: this runner's
-    const uint32_t* halves_at = nullptr;
-    void walk_launch(int64_t nwalks, int* score_out = nullptr, int* corr_out = nullptr) {
-        stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
-        if (rec_cap == 0) {
-            rec_cap = std::max<int64_t>(1 << 16, 2 * nwalks);
-            rec.reserve(static_cast<size_t>(rec_cap) * wp.rec_words);
-        }
-        WalkParams P = wp;
-        P.nwalks = nwalks;
-        P.halves = halves_at ? halves_at : halves.p;
-        P.rec = rec.p;
-        P.rec_cap = rec_cap;
-        P.rec_count = rec_count.p;
-        P.walk_next = rec_count.p + 1;
-        P.walk_stats = stats.p;
-        const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(grid_cap, (nwalks + P.walks_per_block - 1) / P.walks_per_block)));
-        LABS_CUDA(cudaMemsetAsync(rec_count.p, 0, 2 * sizeof(unsigned long long), st));
-        LABS_CUDA(cudaEventRecord(ev[0], st));
-        LABS_CUDA(launch_saw_walk(P, grid, st, score_out, corr_out));
-        LABS_CUDA(cudaEventRecord(ev[1], st));
-        h_count.reserve(1);
-        LABS_CUDA(cudaMemcpyAsync(h_count.p, rec_count.p, sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, st));
-        // the per-walk stats do not depend on the record count: drain them meanwhile
-        h_stats.reserve(static_cast<size_t>(nwalks) * kWalkStatWords);
-        LABS_CUDA(cudaMemcpyAsync(h_stats.p, stats.p,
-                                  static_cast<size_t>(nwalks) * kWalkStatWords * 8,
-                                  cudaMemcpyDeviceToHost, st));
-    }
-
-    // Wait for the launch, copy back records + stats; a record-buffer overflow grows the
-    // buffer and reruns the (deterministic) walks.
-    void walk_finish(int64_t nwalks, BatchOut& out, int* score_out = nullptr, int* corr_out = nullptr) {
-        for (int attempt = 0; attempt < 3; ++attempt) {
-            if (attempt > 0) walk_launch(nwalks, score_out, corr_out);
-            LABS_CUDA(cudaStreamSynchronize(st));
-            const unsigned long long cnt = *h_count.p;
-            float ms = 0;
-            LABS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-            out.kernel_ms += ms;
-            if (static_cast<int64_t>(cnt) > rec_cap) {  // overflow: grow and rerun (deterministic)
-                rec_cap = static_cast<int64_t>(cnt) + cnt / 4 + 1024;
-                rec.reserve(static_cast<size_t>(rec_cap) * wp.rec_words);
-                continue;
-            }
-            out.nrec = static_cast<int64_t>(cnt);
-            out.rec.resize(static_cast<size_t>(cnt) * wp.rec_words);
-            out.stats.resize(static_cast<size_t>(nwalks) * kWalkStatWords);
-            if (cnt) {
-                h_rec.reserve(out.rec.size());
-                LABS_CUDA(cudaMemcpyAsync(h_rec.p, rec.p, out.rec.size() * 4,
-                                          cudaMemcpyDeviceToHost, st));
-                LABS_CUDA(cudaStreamSynchronize(st));
-                std::memcpy(out.rec.data(), h_rec.p, out.rec.size() * 4);
-            }
-            std::memcpy(out.stats.data(), h_stats.p, out.stats.size() * 8);
-            out.d2h += static_cast<int64_t>(sizeof cnt + out.rec.size() * 4 + out.stats.size() * 8);
-            return;
-        }
-        throw CudaFailure("record buffer overflow persisted");
-    }
-};
-
-// Device contexts (stream, events, uploaded hash tables, grow-only batch buffers) are kept
+// Device contexts (streams, events, uploaded hash tables, grow-only job buffers) are kept
 // across run_saw_pool calls with the same walk geometry, so a call pays no allocation or
 // table upload when the configuration repeats (the pipeline calls Step 1 once per round).
 // (heap-allocated and never destroyed: no CUDA calls from static destructors at exit)
@@ -370,33 +78,6 @@ std::string walk_params_for(const Derived& d, bool count_visited, bool debug, Wa
     wp.count_visited = count_visited ? 1 : 0;
     wp.debug_check = debug ? 1 : 0;
     return err;
-}
-
-// Record views of a batch sorted by (walk, iteration); `start[w]..start[w+1]` indexes walk w.
-struct GroupedRecords {
-    std::vector<WalkRecordView> recs;
-    std::vector<int64_t> start;
-    const WalkRecordView* begin(int64_t w) const { return recs.data() + start[static_cast<size_t>(w)]; }
-    const WalkRecordView* end(int64_t w) const { return recs.data() + start[static_cast<size_t>(w) + 1]; }
-};
-
-GroupedRecords group_records(const BatchOut& b, int rec_words, int64_t nwalks) {
-    GroupedRecords g;
-    g.recs.resize(static_cast<size_t>(b.nrec));
-    g.start.assign(static_cast<size_t>(nwalks) + 1, 0);
-    for (int64_t i = 0; i < b.nrec; ++i) {
-        const uint32_t* r = &b.rec[static_cast<size_t>(i) * rec_words];
-        g.recs[static_cast<size_t>(i)] = WalkRecordView{
-            static_cast<int64_t>(r[0]), static_cast<int64_t>(r[1]),
-            static_cast<int64_t>(static_cast<int32_t>(r[2])),
-            static_cast<uint64_t>(r[4]) | (static_cast<uint64_t>(r[5]) << 32), r + kRecHeader};
-        ++g.start[static_cast<size_t>(r[0]) + 1];
-    }
-    std::sort(g.recs.begin(), g.recs.end(), [](const WalkRecordView& a, const WalkRecordView& c) {
-        return a.walk != c.walk ? a.walk < c.walk : a.iteration < c.iteration;
-    });
-    for (int64_t w = 0; w < nwalks; ++w) g.start[static_cast<size_t>(w) + 1] += g.start[static_cast<size_t>(w)];
-    return g;
 }
 
 void half_bits_to_signs(const uint32_t* bits, int kp1, int8_t* half) {
@@ -555,8 +236,359 @@ std::vector<uint32_t> walker_list(const labs_saw_config& cfg, const Derived& d, 
     return out;
 }
 
-constexpr int64_t kMaxBatchWalks = 1 << 20;
-constexpr int64_t kPipelineBatches = 8;  // single-device pool: batches per call (at least 2 waves each)
+constexpr int64_t kMaxBatchWalks = 1 << 20;  // walks per job (bounds the slot buffers)
+constexpr int64_t kPipelineBatches = 8;      // independent pools: jobs per device (>= 2 waves each)
+constexpr int64_t kQueueDepth = 3;           // jobs queued per device ahead of the replay
+constexpr double kBatchTargetMs = 100.0;     // coupled pools: one batch runs about this long
+
+// One run_saw_pool call.
+//
+// Independent pools (no quota / time / stop_at_energy, max_restarts > 0): every (walker,
+// restart) walk depends only on (seed, walker, restart, prefixes[w mod P]) (SURVEY.md
+// §8(e)), so the walkers are split over the devices by restriction class, each device runs
+// its walker-major job list, and the replay merges the devices' walks back into the
+// reference's --threads 1 order (walker, restart, iteration): the candidate list is
+// identical to the reference's for any device count.
+//
+// Coupled pools (quota, stop_at_energy, time budget or unlimited restarts) couple the
+// walkers through the stop flag (saw.cpp:153-170,204-208).  The pool is issued in batches
+// of about kBatchTargetMs (sized from the measured walk rate, and from the remaining time
+// budget), two in flight; the stop conditions are evaluated in delivery order between
+// walks, exactly where the reference checks them, and a stop cancels the batches still
+// running.  With threads <= 1 the batches follow the --threads 1 order exactly (walker 0's
+// restarts first; with unlimited restarts that is walker 0 alone, as in the reference).
+// With threads > 1 every walker runs concurrently, as the reference's pool does when
+// threads >= walkers (saw.cpp:242-257): each batch gives every unfinished walker its next
+// restarts, round-robin, across all devices.
+class Pool {
+public:
+    Pool(const labs_saw_config& cfg, const Derived& d, const WalkParams& wp, SinkChain& sink,
+         PoolAccum& acc)
+        : cfg_(cfg), d_(d), wp_(wp), sink_(sink), acc_(acc) {}
+
+    ~Pool() { shutdown(true); }
+
+    void run(int first, int ndev_use, int ngpu, const std::vector<uint32_t>& walkers,
+             const std::chrono::steady_clock::time_point t0) {
+        t0_ = t0;
+        walkers_ = walkers;
+        ngpu_ = ngpu;
+        owner_.resize(walkers_.size());
+        gen_.resize(walkers_.size());
+        dev_walkers_.assign(static_cast<size_t>(ngpu), {});
+        for (size_t i = 0; i < walkers_.size(); ++i) {
+            const int g = static_cast<int>((walkers_[i] % static_cast<uint32_t>(d_.nprefix)) %
+                                           static_cast<uint32_t>(ngpu));
+            owner_[i] = g;
+            gen_[i] = static_cast<uint32_t>(dev_walkers_[static_cast<size_t>(g)].size());
+            dev_walkers_[static_cast<size_t>(g)].push_back(i);
+        }
+        for (int g = 0; g < ngpu; ++g) {
+            runners_.push_back(acquire_runner(first + g % ndev_use, wp_));
+            DeviceRunner& dr = *runners_.back();
+            dr.seed = cfg_.seed;
+            dr.d = &d_;
+            dr.reserve_generators(dev_walkers_[static_cast<size_t>(g)].size());
+        }
+        for (auto& r : runners_) {
+            ex_.emplace_back(new Executor(*r));
+            ex_.back()->start();
+        }
+        cur_.resize(static_cast<size_t>(ngpu));
+        dev_kernel_ms_.assign(static_cast<size_t>(ngpu), 0.0);
+        dev_seed_ms_.assign(static_cast<size_t>(ngpu), 0.0);
+        const bool coupled = cfg_.candidate_quota > 0 || cfg_.stop_at_energy > 0 ||
+                             cfg_.time_budget_s > 0 || cfg_.max_restarts == 0;
+        if (coupled) run_coupled();
+        else run_independent();
+        for (int g = 0; g < ngpu; ++g) {  // device time = the slowest device
+            acc_.st.kernel_ms = std::max(acc_.st.kernel_ms, dev_kernel_ms_[static_cast<size_t>(g)]);
+            acc_.st.seed_ms = std::max(acc_.st.seed_ms, dev_seed_ms_[static_cast<size_t>(g)]);
+        }
+    }
+
+    // Cancel whatever still runs, join the executors, return the runners to the pool
+    // (only after a clean run: a failed device's state may be unusable).
+    void shutdown(bool failed) {
+        if (done_) return;
+        done_ = true;
+        for (auto& e : ex_) e->cancel();
+        for (auto& e : ex_) e->stop();
+        sink_.flush();  // before the jobs' record buffers are released
+        cur_.clear();
+        retired_.clear();
+        ex_.clear();
+        if (!failed) release_runners(runners_);
+        runners_.clear();
+    }
+
+private:
+    const labs_saw_config& cfg_;
+    const Derived& d_;
+    WalkParams wp_;
+    SinkChain& sink_;
+    PoolAccum& acc_;
+    std::chrono::steady_clock::time_point t0_;
+    int ngpu_ = 1;
+    bool done_ = false;
+    std::vector<uint32_t> walkers_;
+    std::vector<int> owner_;                        // per walker index: device
+    std::vector<uint32_t> gen_;                     // per walker index: generator slot
+    std::vector<std::vector<size_t>> dev_walkers_;  // per device: walker indices, in order
+    std::vector<std::unique_ptr<DeviceRunner>> runners_;
+    std::vector<std::unique_ptr<Executor>> ex_;
+    struct Cursor {
+        JobOut job;
+        bool have = false;
+        int64_t i = 0;
+    };
+    std::vector<Cursor> cur_;
+    std::vector<JobOut> retired_;  // replayed jobs whose records the sink may still reference
+    std::vector<double> dev_kernel_ms_, dev_seed_ms_;
+    double ms_per_walk_ = 0;       // measured device time per walk at full residency
+    double replay_ms_per_walk_ = 0;  // measured host replay time per walk (coupled pools)
+    double wait_ms_ = 0;             // time the replay spent waiting for the devices
+    int64_t last_batch_ = 1;         // walks of the latest coupled batch
+    const bool timing_ = std::getenv("LABS_TIMING") != nullptr;
+    // independent pools: per device, the next walk of its job list
+    struct Gen {
+        size_t k = 0;   // index into dev_walkers_[g]
+        int64_t r = 0;
+    };
+    std::vector<Gen> feed_;
+    std::vector<int64_t> chunk_;
+
+    bool stopped() const { return sink_.stop || sink_.aborted || acc_.diverged != 0; }
+
+    bool deadline_hit() const {
+        return cfg_.time_budget_s > 0 &&
+               std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count() >=
+                   cfg_.time_budget_s;
+    }
+
+    Segment seg(size_t wi, int64_t r0, int64_t r1) const {
+        Segment s;
+        s.walker = walkers_[wi];
+        s.r0 = r0;
+        s.r1 = r1;
+        s.gen = gen_[wi];
+        return s;
+    }
+
+    // ---- independent pools
+    void top_up() {
+        if (feed_.empty()) return;
+        const int64_t R = cfg_.max_restarts;
+        for (int g = 0; g < ngpu_; ++g) {
+            Executor& e = *ex_[static_cast<size_t>(g)];
+            Gen& f = feed_[static_cast<size_t>(g)];
+            const auto& wl = dev_walkers_[static_cast<size_t>(g)];
+            const int64_t chunk = chunk_[static_cast<size_t>(g)];
+            while (e.pushed() - e.popped() < kQueueDepth && f.k < wl.size()) {
+                Job job;
+                while (job.nwalks < chunk && f.k < wl.size()) {
+                    const int64_t take = std::min(R - f.r, chunk - job.nwalks);
+                    job.segs.push_back(seg(wl[f.k], f.r, f.r + take));
+                    job.nwalks += take;
+                    f.r += take;
+                    if (f.r == R) {
+                        ++f.k;
+                        f.r = 0;
+                    }
+                }
+                e.push(std::move(job));
+            }
+        }
+    }
+
+    void run_independent() {
+        const int64_t R = cfg_.max_restarts;
+        const char* nb_env = std::getenv("LABS_PIPELINE_BATCHES");  // (A/B knob)
+        const int64_t nb = std::max<int64_t>(1, nb_env ? std::atoll(nb_env) : kPipelineBatches);
+        feed_.assign(static_cast<size_t>(ngpu_), Gen{});
+        chunk_.assign(static_cast<size_t>(ngpu_), 1);
+        for (int g = 0; g < ngpu_; ++g) {
+            const int64_t total = static_cast<int64_t>(dev_walkers_[static_cast<size_t>(g)].size()) * R;
+            const int64_t resident = runners_[static_cast<size_t>(g)]->resident;
+            chunk_[static_cast<size_t>(g)] = std::max<int64_t>(1, std::min<int64_t>(
+                kMaxBatchWalks, nb == 1 ? total : std::max<int64_t>(2 * resident, (total + nb - 1) / nb)));
+        }
+        top_up();
+        for (size_t wi = 0; wi < walkers_.size() && !stopped(); ++wi)
+            for (int64_t r = 0; r < R && !stopped(); ++r) deliver_next(wi, r);
+    }
+
+    // ---- coupled pools
+    void run_coupled() {
+        const bool exact = cfg_.threads <= 1;
+        const int64_t lim = cfg_.max_restarts > 0 ? cfg_.max_restarts : INT64_MAX;
+        std::vector<int64_t> next_r(walkers_.size(), 0);
+        size_t ex_wi = 0, cyc = 0;
+        int64_t ex_r = 0;
+        int64_t resident_all = 0;
+        for (auto& r : runners_) resident_all += r->resident;
+        std::deque<std::vector<size_t>> issued;  // per batch: walker index of each segment
+        std::deque<std::vector<Segment>> issued_segs;
+        bool exhausted = false;
+        const auto make_batch = [&](int64_t n, std::vector<size_t>& idx, std::vector<Segment>& segs) {
+            int64_t nw = 0;
+            if (exact) {
+                while (nw < n && ex_wi < walkers_.size()) {
+                    const int64_t take = std::min(lim - ex_r, n - nw);
+                    idx.push_back(ex_wi);
+                    segs.push_back(seg(ex_wi, ex_r, ex_r + take));
+                    nw += take;
+                    ex_r += take;
+                    if (ex_r >= lim) {
+                        ++ex_wi;
+                        ex_r = 0;
+                    }
+                }
+                return nw;
+            }
+            int64_t active = 0;
+            for (size_t i = 0; i < walkers_.size(); ++i) active += next_r[i] < lim ? 1 : 0;
+            if (active == 0) return int64_t(0);
+            const int64_t c = std::max<int64_t>(1, n / active);
+            for (size_t step = 0; step < walkers_.size() && nw < n; ++step) {
+                const size_t i = (cyc + step) % walkers_.size();
+                if (next_r[i] >= lim) continue;
+                const int64_t take = std::min({c, lim - next_r[i], n - nw});
+                idx.push_back(i);
+                segs.push_back(seg(i, next_r[i], next_r[i] + take));
+                next_r[i] += take;
+                nw += take;
+                if (nw >= n) cyc = (i + 1) % walkers_.size();
+            }
+            return nw;
+        };
+        // (the first batch is issued even when device setup used up a tiny budget: the
+        // reference's walkers all start their first walk at once)
+        bool first_batch = true;
+        const auto issue = [&]() {
+            if (exhausted || stopped() || (deadline_hit() && !first_batch)) return false;
+            first_batch = false;
+            double target = kBatchTargetMs;
+            if (cfg_.time_budget_s > 0) {
+                const double left = cfg_.time_budget_s * 1e3 -
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+                target = std::min(target, std::max(1.0, left / 3));
+            }
+            // The pipeline runs at the slower of the devices and the host replay (a loose
+            // threshold makes the replay -- dedup of every hit -- the bound).  The first
+            // batches are small (one walk per walker, at most one wave) so that the rates are
+            // measured before the batches grow (at most 4x per batch) to ~target ms.
+            int64_t n = std::min<int64_t>(resident_all, static_cast<int64_t>(walkers_.size()));
+            if (ms_per_walk_ > 0) {
+                n = std::max<int64_t>(resident_all, static_cast<int64_t>(ngpu_ * target / ms_per_walk_));
+                if (replay_ms_per_walk_ > 0)
+                    n = std::min<int64_t>(n, static_cast<int64_t>(target / replay_ms_per_walk_));
+                n = std::max<int64_t>(1, std::min<int64_t>(n, 4 * last_batch_));
+            }
+            n = std::min<int64_t>(n, kMaxBatchWalks * ngpu_);
+            std::vector<size_t> idx;
+            std::vector<Segment> segs;
+            last_batch_ = make_batch(n, idx, segs);
+            if (last_batch_ == 0) {
+                exhausted = true;
+                return false;
+            }
+            std::vector<Job> jobs(static_cast<size_t>(ngpu_));
+            for (size_t j = 0; j < segs.size(); ++j) {
+                Job& job = jobs[static_cast<size_t>(owner_[idx[j]])];
+                job.segs.push_back(segs[j]);
+                job.nwalks += segs[j].r1 - segs[j].r0;
+            }
+            for (int g = 0; g < ngpu_; ++g)
+                if (jobs[static_cast<size_t>(g)].nwalks > 0)
+                    ex_[static_cast<size_t>(g)]->push(std::move(jobs[static_cast<size_t>(g)]));
+            if (timing_)
+                std::fprintf(stderr, "[labs] t=%.1f ms issue batch of %lld walks (%zu segs; device %.4f, "
+                             "replay %.4f ms/walk)\n",
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count(),
+                             static_cast<long long>(last_batch_), segs.size(), ms_per_walk_, replay_ms_per_walk_);
+            issued.push_back(std::move(idx));
+            issued_segs.push_back(std::move(segs));
+            return true;
+        };
+        while (issued.size() < 2 && issue()) {
+        }
+        while (!issued.empty() && !stopped()) {
+            const std::vector<size_t> idx = std::move(issued.front());
+            const std::vector<Segment> segs = std::move(issued_segs.front());
+            issued.pop_front();
+            issued_segs.pop_front();
+            const auto ta = std::chrono::steady_clock::now();
+            const double wait0 = wait_ms_;
+            int64_t nw = 0;
+            for (size_t j = 0; j < segs.size() && !stopped(); ++j)
+                for (int64_t r = segs[j].r0; r < segs[j].r1 && !stopped(); ++r, ++nw)
+                    deliver_next(idx[j], r);
+            // host replay time per walk (the waits for the devices excluded)
+            if (nw > 0)
+                replay_ms_per_walk_ = std::max(0.0, std::chrono::duration<double, std::milli>(
+                    std::chrono::steady_clock::now() - ta).count() - (wait_ms_ - wait0)) /
+                    static_cast<double>(nw);
+            while (issued.size() < 2 && issue()) {
+            }
+        }
+    }
+
+    // ---- replay: the next walk of walker index wi (restart r) from its device's jobs
+    void deliver_next(size_t wi, int64_t r) {
+        const int g = owner_[wi];
+        Cursor& c = cur_[static_cast<size_t>(g)];
+        while (!c.have || c.i >= static_cast<int64_t>(c.job.walk_walker.size())) {
+            if (c.have) {
+                retired_.push_back(std::move(c.job));
+                c.have = false;
+            }
+            top_up();
+            const auto tw = std::chrono::steady_clock::now();
+            c.job = ex_[static_cast<size_t>(g)]->pop();
+            wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
+            c.have = true;
+            c.i = 0;
+            account(g, c.job);
+            if (retired_.size() >= 2) {
+                sink_.flush();
+                retired_.clear();
+            }
+        }
+        const int64_t i = c.i++;
+        const JobOut& b = c.job;
+        if (b.walk_walker[static_cast<size_t>(i)] != walkers_[wi] ||
+            b.walk_restart[static_cast<size_t>(i)] != r)
+            throw CudaFailure("walk replay out of order");
+        const int64_t* s = &b.stats[static_cast<size_t>(i) * kWalkStatWords];
+        for (int64_t v = b.start[static_cast<size_t>(i)]; v < b.start[static_cast<size_t>(i) + 1]; ++v)
+            sink_.deliver(walkers_[wi], r, b.views[static_cast<size_t>(v)]);
+        ++acc_.st.walks;
+        acc_.st.iterations += s[kWsIterations];
+        acc_.st.emitted_raw += s[kWsEmitted];
+        acc_.st.delta_evals += s[kWsDeltaEvals] >= 0 ? s[kWsDeltaEvals] : 0;
+        acc_.st.exhausted_walks += s[kWsExhausted];
+        acc_.st.wide_iterations += s[kWsWideIters];
+        acc_.diverged += s[kWsDiverged];
+        // offer_best (saw.cpp:160-169)
+        if (!acc_.best_set || s[kWsBest] < acc_.st.best_energy) {
+            acc_.st.best_energy = s[kWsBest];
+            acc_.best_set = true;
+            if (cfg_.stop_at_energy > 0 && s[kWsBest] <= cfg_.stop_at_energy) sink_.stop = true;
+        }
+    }
+
+    void account(int g, const JobOut& b) {
+        dev_kernel_ms_[static_cast<size_t>(g)] += b.kernel_ms;
+        dev_seed_ms_[static_cast<size_t>(g)] += b.seed_ms;
+        acc_.st.h2d_bytes += b.h2d;
+        acc_.st.d2h_bytes += b.d2h;
+        const int64_t nw = static_cast<int64_t>(b.walk_walker.size());
+        const int64_t res = runners_[static_cast<size_t>(g)]->resident;
+        if (nw > 0 && b.kernel_ms > 0)
+            ms_per_walk_ = b.kernel_ms / static_cast<double>(std::max(nw, res));
+    }
+};
 
 int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_batch_fn emit_batch,
              void* user, labs_pool_stats* out) {
@@ -579,19 +611,18 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
         return LABS_ENODEV;
     }
     const int first = std::max(0, cfg.device);
-    // n_gpus class shards run concurrently, shard g on device first + g (mod the devices
-    // available from `first`); more shards than devices share a device (separate streams)
-    const int ngpu = std::max(1, cfg.n_gpus);
-    const int ndev_use = std::max(1, ndev_avail - first);
     if (first >= ndev_avail) {
         set_error("device ordinal out of range");
         return LABS_ENODEV;
     }
+    // n_gpus class shards run concurrently, shard g on device first + g (mod the devices
+    // available from `first`); more shards than devices share a device (separate streams)
+    const int ngpu = std::max(1, cfg.n_gpus);
+    const int ndev_use = std::max(1, ndev_avail - first);
     const int sidx = cfg.shard_count > 1 ? cfg.shard_index : 0;
     const int scnt = cfg.shard_count > 1 ? cfg.shard_count : 1;
-    const std::vector<uint32_t> walkers = walker_list(cfg, d, sidx, scnt);
-    const bool coupled = cfg.candidate_quota > 0 || cfg.stop_at_energy > 0 ||
-                         cfg.time_budget_s > 0 || cfg.max_restarts == 0;
+    std::vector<uint32_t> walkers = walker_list(cfg, d, sidx, scnt);
+    if (cfg.max_restarts < 0) walkers.clear();  // (saw.cpp:202: no restart runs)
 
     PoolAccum acc;
     SinkChain sink{};
@@ -600,319 +631,21 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
     sink.emit = emit;
     sink.emit_batch = emit_batch;
     sink.user = user;
-    std::vector<std::unique_ptr<DeviceRunner>> runners;
-    try {
-        for (int g = 0; g < (coupled ? 1 : ngpu); ++g)
-            runners.push_back(acquire_runner(first + g % ndev_use, wp));
-        // ---- build the ordered walk sequence as batches of segments ----
-        // Per walker: state carried across batches (only in coupled mode can a walker's
-        // restarts span batches).
-        const auto deadline_hit = [&]() {
-            return cfg.time_budget_s > 0 &&
-                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >=
-                       cfg.time_budget_s;
-        };
-        auto process_batch = [&](const std::vector<Segment>& segs, BatchOut& b) {
-            const int64_t nw = static_cast<int64_t>(b.walk_walker.size());
-            const auto groups = group_records(b, wp.rec_words, nw);
-            for (int64_t i = 0; i < nw && !sink.stop && !sink.aborted; ++i) {
-                const int64_t* s = &b.stats[static_cast<size_t>(i) * kWalkStatWords];
-                for (const WalkRecordView* r = groups.begin(i); r != groups.end(i); ++r)
-                    sink.deliver(static_cast<uint32_t>(b.walk_walker[i]), b.walk_restart[i], *r);
-                ++acc.st.walks;
-                acc.st.iterations += s[kWsIterations];
-                acc.st.emitted_raw += s[kWsEmitted];
-                acc.st.delta_evals += s[kWsDeltaEvals] >= 0 ? s[kWsDeltaEvals] : 0;
-                acc.st.exhausted_walks += s[kWsExhausted];
-                acc.st.wide_iterations += s[kWsWideIters];
-                acc.diverged += s[kWsDiverged];
-                // offer_best (saw.cpp:160-169)
-                if (!acc.best_set || s[kWsBest] < acc.st.best_energy) {
-                    acc.st.best_energy = s[kWsBest];
-                    acc.best_set = true;
-                    if (cfg.stop_at_energy > 0 && s[kWsBest] <= cfg.stop_at_energy) sink.stop = true;
-                }
-                if (acc.diverged) break;
-            }
-            sink.flush();  // the batch's record buffer dies with `b`
-            (void)segs;
-        };
-
-        if (!coupled) {
-            // Every (walker, restart) walk is independent: split walkers across GPUs by
-            // restriction class, run each GPU's list in batches, merge in walker order.
-            const int64_t R = cfg.max_restarts;
-            std::vector<std::vector<uint32_t>> per_dev(static_cast<size_t>(ngpu));
-            for (uint32_t w : walkers)
-                per_dev[static_cast<size_t>((w % static_cast<uint32_t>(d.nprefix)) % ngpu)].push_back(w);
-            std::vector<std::vector<BatchOut>> outs(static_cast<size_t>(ngpu));
-            std::vector<std::vector<std::vector<Segment>>> segs_all(static_cast<size_t>(ngpu));
-            std::vector<std::string> errs(static_cast<size_t>(ngpu));
-            // batches: whole walkers while they fit, else restart ranges
-            const auto make_batches = [&](const std::vector<uint32_t>& wl, int64_t max_walks) {
-                std::vector<std::vector<Segment>> batches;
-                std::vector<Segment> cur;
-                int64_t cur_walks = 0;
-                for (uint32_t w : wl) {
-                    int64_t r = 0;
-                    while (r < R) {
-                        const int64_t take = std::min(R - r, max_walks - cur_walks);
-                        cur.push_back(Segment{w, r, r + take});
-                        cur_walks += take;
-                        r += take;
-                        if (cur_walks == max_walks) {
-                            batches.push_back(std::move(cur));
-                            cur.clear();
-                            cur_walks = 0;
-                        }
-                    }
-                }
-                if (!cur.empty()) batches.push_back(std::move(cur));
-                return batches;
-            };
-            // Seed one batch on `dr` (K3); a walker split across batches continues from the
-            // generator state its previous batch ended with.
-            struct Carry {
-                uint32_t walker = 0xffffffffu;
-                std::array<uint64_t, 4> state{};
-            };
-            const auto seed_batch = [&](DeviceRunner& dr, const std::vector<Segment>& segs, Carry& carry,
-                                        BatchOut& b) {
-                std::vector<std::array<uint64_t, 4>> states(segs.size());
-                std::vector<int32_t> init(segs.size(), 1);
-                int64_t nw = 0;
-                for (size_t i = 0; i < segs.size(); ++i) {
-                    if (segs[i].r0 > 0 && segs[i].walker == carry.walker) {
-                        init[i] = 0;
-                        states[i] = carry.state;
-                    }
-                    for (int64_t r = segs[i].r0; r < segs[i].r1; ++r) {
-                        b.walk_walker.push_back(segs[i].walker);
-                        b.walk_restart.push_back(r);
-                    }
-                    nw += segs[i].r1 - segs[i].r0;
-                }
-                dr.seed(segs, d, cfg.seed, states, init, nw, b);
-                carry.walker = segs.back().walker;
-                carry.state = states.back();
-                return nw;
-            };
-            auto dev_job = [&](int g) {
-                try {
-                    DeviceRunner& dr = *runners[static_cast<size_t>(g)];
-                    LABS_CUDA(cudaSetDevice(dr.dev));
-                    Carry carry;
-                    for (auto& segs : make_batches(per_dev[static_cast<size_t>(g)], kMaxBatchWalks)) {
-                        BatchOut b;
-                        const auto tA = std::chrono::steady_clock::now();
-                        const int64_t nw = seed_batch(dr, segs, carry, b);
-                        const auto tB = std::chrono::steady_clock::now();
-                        dr.walk(nw, b);
-                        const auto tC = std::chrono::steady_clock::now();
-                        if (std::getenv("LABS_TIMING"))
-                            std::fprintf(stderr, "[labs] seed %.2f ms, walk+d2h %.2f ms (kernel %.2f)\n",
-                                         std::chrono::duration<double, std::milli>(tB - tA).count(),
-                                         std::chrono::duration<double, std::milli>(tC - tB).count(),
-                                         b.kernel_ms);
-                        outs[static_cast<size_t>(g)].push_back(std::move(b));
-                        segs_all[static_cast<size_t>(g)].push_back(segs);
-                    }
-                } catch (const std::exception& e) {
-                    errs[static_cast<size_t>(g)] = e.what();
-                }
-            };
-            if (ngpu == 1) {
-                // One device: the walks run as a pipeline of batches on two runners (two
-                // streams and buffer sets).  While batch i runs -- and fills the SMs its
-                // predecessor's tail leaves idle -- the host replays batch i-1 into the sink.
-                runners.push_back(acquire_runner(first, wp));
-                DeviceRunner* slot[2] = {runners[0].get(), runners[1].get()};
-                LABS_CUDA(cudaSetDevice(slot[0]->dev));
-                const int64_t resident = static_cast<int64_t>(slot[0]->grid_cap) * wp.walks_per_block;
-                const int64_t total = static_cast<int64_t>(walkers.size()) * R;
-                const char* nb_env = std::getenv("LABS_PIPELINE_BATCHES");  // (A/B knob)
-                const int64_t nb = std::max<int64_t>(1, nb_env ? std::atoll(nb_env) : kPipelineBatches);
-                const int64_t chunk = std::min<int64_t>(
-                    kMaxBatchWalks, nb == 1 ? total : std::max<int64_t>(2 * resident, (total + nb - 1) / nb));
-                const auto batches = make_batches(walkers, chunk);
-                std::vector<BatchOut> bo(batches.size());
-                std::vector<int64_t> nws(batches.size()), off(batches.size());
-                // K3 once for the whole pool (walker order = batch order), so no batch waits on
-                // a seed launch queued behind the other stream's walk kernel
-                {
-                    std::vector<Segment> all;
-                    for (uint32_t w : walkers) all.push_back(Segment{w, 0, R});
-                    std::vector<std::array<uint64_t, 4>> states(all.size());
-                    std::vector<int32_t> init(all.size(), 1);
-                    BatchOut sb;
-                    slot[0]->seed(all, d, cfg.seed, states, init, total, sb);
-                    acc.st.seed_ms += sb.seed_ms;
-                    acc.st.h2d_bytes += sb.h2d;
-                    acc.st.d2h_bytes += sb.d2h;
-                }
-                int64_t o = 0;
-                for (size_t i = 0; i < batches.size(); ++i) {
-                    off[i] = o;
-                    nws[i] = 0;
-                    for (const Segment& sg : batches[i]) {
-                        for (int64_t r = sg.r0; r < sg.r1; ++r) {
-                            bo[i].walk_walker.push_back(sg.walker);
-                            bo[i].walk_restart.push_back(r);
-                        }
-                        nws[i] += sg.r1 - sg.r0;
-                    }
-                    o += nws[i];
-                }
-                const auto tD = std::chrono::steady_clock::now();
-                double replay_ms = 0;
-                const auto retire = [&](size_t j) {  // wait for batch j, replay it, free it
-                    slot[j % 2]->walk_finish(nws[j], bo[j]);
-                    acc.st.kernel_ms += bo[j].kernel_ms;
-                    acc.st.seed_ms += bo[j].seed_ms;
-                    acc.st.h2d_bytes += bo[j].h2d;
-                    acc.st.d2h_bytes += bo[j].d2h;
-                    const auto t = std::chrono::steady_clock::now();
-                    if (!sink.aborted && acc.diverged == 0) process_batch(batches[j], bo[j]);
-                    replay_ms += std::chrono::duration<double, std::milli>(
-                        std::chrono::steady_clock::now() - t).count();
-                    bo[j] = BatchOut();
-                };
-                size_t launched = 0, retired = 0;
-                for (size_t i = 0; i < batches.size(); ++i) {
-                    if (i >= 2) retire(retired++);  // batch i - 2: frees slot i % 2
-                    if (sink.aborted || acc.diverged) break;
-                    slot[i % 2]->halves_at = slot[0]->halves.p + static_cast<size_t>(off[i]) * wp.hw;
-                    slot[i % 2]->walk_launch(nws[i]);
-                    launched = i + 1;
-                }
-                while (retired < launched) retire(retired++);
-                slot[0]->halves_at = slot[1]->halves_at = nullptr;
-                if (std::getenv("LABS_TIMING"))
-                    std::fprintf(stderr, "[labs] %zu pipelined batches of <= %lld walks: %.2f ms, "
-                                 "host replay %.2f ms (overlapped)\n", batches.size(),
-                                 static_cast<long long>(chunk),
-                                 std::chrono::duration<double, std::milli>(
-                                     std::chrono::steady_clock::now() - tD).count(), replay_ms);
-            } else {
-                std::vector<std::thread> th;
-                for (int g = 0; g < ngpu; ++g) th.emplace_back(dev_job, g);
-                for (auto& t : th) t.join();
-            }
-            for (const auto& e : errs)
-                if (!e.empty()) throw CudaFailure(e);
-            if (ngpu > 1) {
-                for (int g = 0; g < ngpu; ++g) {  // device time = slowest device
-                    double kms = 0, sms = 0;
-                    for (const auto& b : outs[static_cast<size_t>(g)]) {
-                        kms += b.kernel_ms;
-                        sms += b.seed_ms;
-                        acc.st.h2d_bytes += b.h2d;
-                        acc.st.d2h_bytes += b.d2h;
-                    }
-                    acc.st.kernel_ms = std::max(acc.st.kernel_ms, kms);
-                    acc.st.seed_ms = std::max(acc.st.seed_ms, sms);
-                }
-                // merge: walks of all devices in (walker, restart) order
-                struct Ref {
-                    uint32_t walker;
-                    int64_t restart;
-                    int g;
-                    size_t b;
-                    int64_t i;
-                };
-                std::vector<Ref> refs;
-                std::vector<std::vector<GroupedRecords>> grp(static_cast<size_t>(ngpu));
-                for (int g = 0; g < ngpu; ++g)
-                    for (size_t bi = 0; bi < outs[static_cast<size_t>(g)].size(); ++bi) {
-                        const BatchOut& b = outs[static_cast<size_t>(g)][bi];
-                        grp[static_cast<size_t>(g)].push_back(
-                            group_records(b, wp.rec_words, static_cast<int64_t>(b.walk_walker.size())));
-                        for (size_t i = 0; i < b.walk_walker.size(); ++i)
-                            refs.push_back(Ref{static_cast<uint32_t>(b.walk_walker[i]), b.walk_restart[i], g, bi,
-                                               static_cast<int64_t>(i)});
-                    }
-                std::sort(refs.begin(), refs.end(), [](const Ref& a, const Ref& c) {
-                    return a.walker != c.walker ? a.walker < c.walker : a.restart < c.restart;
-                });
-                for (const Ref& r : refs) {
-                    const BatchOut& b = outs[static_cast<size_t>(r.g)][r.b];
-                    const int64_t* s = &b.stats[static_cast<size_t>(r.i) * kWalkStatWords];
-                    const GroupedRecords& gr = grp[static_cast<size_t>(r.g)][r.b];
-                    for (const WalkRecordView* v = gr.begin(r.i); v != gr.end(r.i); ++v)
-                        sink.deliver(r.walker, r.restart, *v);
-                    ++acc.st.walks;
-                    acc.st.iterations += s[kWsIterations];
-                    acc.st.emitted_raw += s[kWsEmitted];
-                    acc.st.delta_evals += s[kWsDeltaEvals] >= 0 ? s[kWsDeltaEvals] : 0;
-                    acc.st.exhausted_walks += s[kWsExhausted];
-                    acc.st.wide_iterations += s[kWsWideIters];
-                    acc.diverged += s[kWsDiverged];
-                    if (!acc.best_set || s[kWsBest] < acc.st.best_energy) {
-                        acc.st.best_energy = s[kWsBest];
-                        acc.best_set = true;
-                    }
-                }
-                sink.flush();  // before the devices' record buffers are released
-            }
-        } else {
-            // Coupled stop conditions: ordered batches, stop replay exactly like --threads 1.
-            DeviceRunner& dr = *runners[0];
-            int64_t batch_walks = 4096;
-            size_t wi = 0;
-            int64_t next_r = 0;
-            std::array<uint64_t, 4> carry_state{};
-            bool carry_valid = false;
-            while (wi < walkers.size() && !sink.stop && !sink.aborted && acc.diverged == 0) {
-                if (deadline_hit()) break;
-                std::vector<Segment> segs;
-                std::vector<std::array<uint64_t, 4>> states;
-                std::vector<int32_t> init;
-                BatchOut b;
-                int64_t nw = 0;
-                size_t wj = wi;
-                int64_t r = next_r;
-                while (nw < batch_walks && wj < walkers.size()) {
-                    const int64_t lim = cfg.max_restarts > 0 ? cfg.max_restarts : INT64_MAX;
-                    const int64_t take = std::min(lim - r, batch_walks - nw);
-                    segs.push_back(Segment{walkers[wj], r, r + take});
-                    states.push_back(carry_state);
-                    init.push_back(r == 0 || !carry_valid ? 1 : 0);
-                    for (int64_t q = r; q < r + take; ++q) {
-                        b.walk_walker.push_back(walkers[wj]);
-                        b.walk_restart.push_back(q);
-                    }
-                    nw += take;
-                    r += take;
-                    if (r >= lim) {
-                        ++wj;
-                        r = 0;
-                        carry_valid = false;
-                    }
-                }
-                dr.seed(segs, d, cfg.seed, states, init, nw, b);
-                if (r > 0) {  // last walker continues in the next batch
-                    carry_state = states.back();
-                    carry_valid = true;
-                }
-                dr.walk(nw, b);
-                acc.st.kernel_ms += b.kernel_ms;
-                acc.st.seed_ms += b.seed_ms;
-                acc.st.h2d_bytes += b.h2d;
-                acc.st.d2h_bytes += b.d2h;
-                process_batch(segs, b);
-                wi = wj;
-                next_r = r;
-                batch_walks = std::min<int64_t>(batch_walks * 2, kMaxBatchWalks);
-            }
+    if (!walkers.empty()) {
+        Pool pool(cfg, d, wp, sink, acc);
+        try {
+            pool.run(first, ndev_use, ngpu, walkers, t0);
+            pool.shutdown(false);
+        } catch (const CudaFailure& e) {
+            pool.shutdown(true);
+            set_error(e.what());
+            return LABS_ECUDA;
+        } catch (const std::bad_alloc&) {
+            pool.shutdown(true);
+            set_error("out of host memory");
+            return LABS_ECUDA;
         }
-    } catch (const CudaFailure& e) {
-        set_error(e.what());
-        return LABS_ECUDA;  // runners dropped: their state may be unusable
-    } catch (const std::bad_alloc&) {
-        set_error("out of host memory");
-        return LABS_ECUDA;
     }
-    release_runners(runners);
     if (acc.diverged) {
         set_error("saw walk energy bookkeeping diverged");
         return LABS_ELOGIC;
@@ -923,7 +656,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
     acc.st.delta_evals = cfg.count_visited ? acc.st.delta_evals : -1;
     int64_t free_bits = d.kp1 - d.p;
     acc.st.delta_evals_computed = (acc.st.iterations + acc.st.walks) * (free_bits > 0 ? free_bits : 0);
-    acc.st.n_gpus = coupled ? 1 : ngpu;
+    acc.st.n_gpus = ngpu;
     acc.st.wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (out) *out = acc.st;
@@ -974,20 +707,22 @@ int walks_from_halves(int L, int p, int64_t t_i, int64_t e_l, double fpr, const 
     wp.count_visited = count ? 1 : 0;
     wp.debug_check = debug ? 1 : 0;
     try {
-        DeviceRunner dr;
-        dr.init(0, wp);
+        std::unique_ptr<DeviceRunner> dr = acquire_runner(0, wp);
         std::vector<uint32_t> hb(static_cast<size_t>(nwalks) * wp.hw, 0u);
         for (int64_t w = 0; w < nwalks; ++w)
             for (int i = 0; i < kp1; ++i)
                 if (halves[w * kp1 + i] > 0) hb[static_cast<size_t>(w) * wp.hw + (i >> 5)] |= 1u << (i & 31);
-        dr.upload_halves(hb, nwalks);
-        BatchOut b;
         DevBuf<int> dscore, dcorr;
         if (deltas_out) {
             dscore.reserve(static_cast<size_t>(nwalks) * kp1);
             dcorr.reserve(static_cast<size_t>(nwalks) * std::max(1, kp1 - 1));
         }
-        dr.walk(nwalks, b, deltas_out ? dscore.p : nullptr, deltas_out ? dcorr.p : nullptr);
+        Job job;
+        job.nwalks = nwalks;
+        job.host_halves = hb.data();
+        job.score_out = deltas_out ? dscore.p : nullptr;
+        job.corr_out = deltas_out ? dcorr.p : nullptr;
+        JobOut b = dr->run_sync(job);
         if (deltas_out) {
             std::vector<int> hs(static_cast<size_t>(nwalks) * kp1), hc(static_cast<size_t>(nwalks) * (kp1 - 1));
             LABS_CUDA(cudaMemcpy(hs.data(), dscore.p, hs.size() * 4, cudaMemcpyDeviceToHost));
@@ -997,7 +732,9 @@ int walks_from_halves(int L, int p, int64_t t_i, int64_t e_l, double fpr, const 
             if (corr_out)
                 for (size_t i = 0; i < hc.size(); ++i) corr_out[i] = hc[i];
         }
-        const auto groups = group_records(b, wp.rec_words, nwalks);
+        std::vector<std::unique_ptr<DeviceRunner>> keep;
+        keep.push_back(std::move(dr));
+        release_runners(keep);
         std::vector<int8_t> half(static_cast<size_t>(kp1));
         for (int64_t w = 0; w < nwalks; ++w) {
             const int64_t* s = &b.stats[static_cast<size_t>(w) * kWalkStatWords];
@@ -1015,9 +752,10 @@ int walks_from_halves(int L, int p, int64_t t_i, int64_t e_l, double fpr, const 
                 r.diverged = s[kWsDiverged];
             }
             if (on_rec)
-                for (const WalkRecordView* v = groups.begin(w); v != groups.end(w); ++v) {
-                    half_bits_to_signs(v->half, kp1, half.data());
-                    if (on_rec(user, w, v->iteration, v->energy, half.data(), kp1) != 0) return LABS_EABORT;
+                for (int64_t v = b.start[static_cast<size_t>(w)]; v < b.start[static_cast<size_t>(w) + 1]; ++v) {
+                    const WalkRecordView& rv = b.views[static_cast<size_t>(v)];
+                    half_bits_to_signs(rv.half, kp1, half.data());
+                    if (on_rec(user, w, rv.iteration, rv.energy, half.data(), kp1) != 0) return LABS_EABORT;
                 }
         }
     } catch (const CudaFailure& e) {
@@ -1178,10 +916,19 @@ int labs_bench_create(const labs_saw_config* cfg, labs_bench_plan** out) {
         bp.dr->init(std::max(0, cfg->device), wp);
         const int sidx = cfg->shard_count > 1 ? cfg->shard_index : 0;
         const int scnt = cfg->shard_count > 1 ? cfg->shard_count : 1;
-        for (uint32_t w : walker_list(bp.cfg, bp.d, sidx, scnt))
-            bp.segs.push_back(Segment{w, 0, cfg->max_restarts});
+        for (uint32_t w : walker_list(bp.cfg, bp.d, sidx, scnt)) {
+            Segment g;
+            g.walker = w;
+            g.r0 = 0;
+            g.r1 = cfg->max_restarts;
+            g.gen = static_cast<uint32_t>(bp.segs.size());
+            bp.segs.push_back(g);
+        }
         bp.nwalks = static_cast<int64_t>(bp.segs.size()) * cfg->max_restarts;
         if (bp.nwalks > kMaxBatchWalks) throw CudaFailure("bench plan larger than one batch");
+        bp.dr->seed = bp.cfg.seed;
+        bp.dr->d = &bp.d;
+        bp.dr->reserve_generators(bp.segs.size());
     } catch (const CudaFailure& e) {
         delete plan;
         set_error(e.what());
@@ -1197,15 +944,15 @@ int labs_bench_run(labs_bench_plan* plan, int32_t reps, double* ms_per_rep, labs
         DeviceRunner& dr = *bp.dr;
         LABS_CUDA(cudaSetDevice(dr.dev));
         double total = 0;
-        BatchOut b;
+        JobOut b;
         bp.l2_scratch.reserve(BenchPlan::kL2Flush);
+        Job job;
+        job.segs = bp.segs;
+        job.nwalks = bp.nwalks;
         for (int r = 0; r < reps; ++r) {
-            LABS_CUDA(cudaMemsetAsync(bp.l2_scratch.p, r & 0xff, BenchPlan::kL2Flush, dr.st));
-            b = BatchOut();
-            std::vector<std::array<uint64_t, 4>> states(bp.segs.size());
-            std::vector<int32_t> init(bp.segs.size(), 1);
-            dr.seed(bp.segs, bp.d, bp.cfg.seed, states, init, bp.nwalks, b);
-            dr.walk(bp.nwalks, b);
+            LABS_CUDA(cudaMemsetAsync(bp.l2_scratch.p, r & 0xff, BenchPlan::kL2Flush, 0));
+            LABS_CUDA(cudaDeviceSynchronize());
+            b = dr.run_sync(job);
             total += b.kernel_ms + b.seed_ms;
         }
         if (ms_per_rep) *ms_per_rep = reps > 0 ? total / reps : 0;
@@ -1225,14 +972,13 @@ int labs_bench_run(labs_bench_plan* plan, int32_t reps, double* ms_per_rep, labs
             }
             // post-dedup count of the last rep's sieve hits
             std::unordered_set<uint64_t> seen;
-            for (int64_t i = 0; i < b.nrec; ++i) {
-                const uint32_t* rr = &b.rec[static_cast<size_t>(i) * dr.wp.rec_words];
-                seen.insert(static_cast<uint64_t>(rr[4]) | (static_cast<uint64_t>(rr[5]) << 32));
-            }
+            for (const WalkRecordView& v : b.views) seen.insert(v.hash);
             st.emitted = static_cast<int64_t>(seen.size());
             st.delta_evals = bp.cfg.count_visited ? st.delta_evals : -1;
             const int64_t free_bits = bp.d.kp1 - bp.d.p;
             st.delta_evals_computed = (st.iterations + st.walks) * free_bits;
+            st.h2d_bytes = b.h2d;
+            st.d2h_bytes = b.d2h;
             st.n_gpus = 1;
             *last = st;
         }

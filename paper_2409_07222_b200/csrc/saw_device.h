@@ -7,6 +7,7 @@ namespace labs_b200 {
 
 constexpr int kMaxR = 16;          // neighbours per lane: free bits <= 32*16 = 512
 constexpr int kMaxHalf = 1024;     // TabulationHash::kMaxLen (rng.hpp:77)
+constexpr unsigned kRingWaitSpins = 5000000u;  // a full ring waits <= ~20 s for a drain
 constexpr int kRecHeader = 6;      // record header: walk, iteration, energy, flags,
                                    // canonical_hash(0) of the full sequence (lo, hi)
 
@@ -41,7 +42,7 @@ struct WalkParams {
     int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)
     int32_t rec_words;             // kRecHeader + hw
     int64_t nwalks;                // walks in this launch
-    int64_t rec_cap;               // record slots in rec
+    int64_t rec_cap;               // record ring slots (a power of two)
     // inputs (device pointers)
     const uint64_t* fm;            // [3][kp1]: tabulation flip masks of half position j in
                                    //   tables 0/1 (Bloom keys), then the flip mask of the
@@ -52,9 +53,19 @@ struct WalkParams {
     uint64_t salt_full;            // table-0 salt for L
     int32_t fm_words;              // u32 words of the block-level fm table in shared memory
     const uint32_t* halves;        // [nwalks][hw] initial half bits (bit i set <=> +1)
-    // outputs
+    // outputs: the sieve's record ring (K2, north_star (d)).  A warp reserves slots for all of
+    // its segments' hits with one atomicAdd on rec_count (the ring head); a slot is written
+    // once rec_count - rec_tail < rec_cap (the host advances rec_tail as it drains the ring
+    // with async copies while the launch runs), and published by its tag (slot + 1, written
+    // after a fence) -- the ring never overflows, so no batch is ever rerun.
     uint32_t* rec;                 // [rec_cap][rec_words]
-    unsigned long long* rec_count; // emissions attempted (may exceed rec_cap => overflow)
+    uint32_t* rec_tag;             // [rec_cap] (uint32)(rec_seq0 + slot + 1) once slot's record
+                                   //   is complete (rec_seq0: records the ring carried in
+                                   //   earlier launches, so stale tags never match)
+    unsigned long long rec_seq0;
+    unsigned long long* rec_count; // ring head: slots reserved in this launch
+    const unsigned long long* rec_tail;  // ring tail: slots the host has drained (host-written)
+    int* ctl;                      // [0] ring abort (no drain for ~20 s), [1] cancel
     unsigned long long* walk_next; // dynamic walk-group queue (zeroed per launch)
     int64_t* walk_stats;           // [nwalks][kWalkStatWords]
 };
@@ -83,7 +94,9 @@ struct SeedParams {
     const int64_t* seg_restarts;   // [nseg]
     const int64_t* seg_offset;     // [nseg] first walk index of the segment in `halves`
     const int32_t* seg_init;       // [nseg] 1 = fresh Rng(seed, walker)
-    uint64_t* rng_state;           // [nseg][4] in/out
+    const uint32_t* seg_slot;      // [nseg] the walker's generator slot in rng_state
+    uint64_t* rng_state;           // [walker slots][4] in/out: a walker's stream continues
+                                   //   across segments (batches) from here
     uint32_t* halves;              // [nwalks][hw]
 };
 

@@ -9,7 +9,9 @@
 namespace labs_b200 {
 
 // ---------------------------------------------------------------------------
-// K3: one thread per walker; restarts drawn in order from the walker's stream.
+// K3: one thread per segment (restarts [r0, r1) of one walker), drawn in order from the
+// walker's stream; the stream state lives in rng_state[seg_slot] between segments, so
+// consecutive batches continue a walker on the device with no host round trip.
 __device__ __forceinline__ uint64_t splitmix64_dev(uint64_t& s) {
     uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -29,10 +31,11 @@ __global__ void saw_seed_kernel(SeedParams P) {
         s2 = splitmix64_dev(sm);
         s3 = splitmix64_dev(sm);
     } else {
-        s0 = P.rng_state[4 * i + 0];
-        s1 = P.rng_state[4 * i + 1];
-        s2 = P.rng_state[4 * i + 2];
-        s3 = P.rng_state[4 * i + 3];
+        const uint64_t* st = P.rng_state + 4 * (size_t)P.seg_slot[i];
+        s0 = st[0];
+        s1 = st[1];
+        s2 = st[2];
+        s3 = st[3];
     }
     const uint32_t pre = P.prefix_bits[i];
     for (int64_t r = 0; r < P.seg_restarts[i]; ++r) {
@@ -62,10 +65,11 @@ __global__ void saw_seed_kernel(SeedParams P) {
         if (P.kp1 & 31) out[P.kp1 >> 5] = word;
         for (int wd = (P.kp1 + 31) >> 5; wd < P.hw; ++wd) out[wd] = 0;
     }
-    P.rng_state[4 * i + 0] = s0;
-    P.rng_state[4 * i + 1] = s1;
-    P.rng_state[4 * i + 2] = s2;
-    P.rng_state[4 * i + 3] = s3;
+    uint64_t* st = P.rng_state + 4 * (size_t)P.seg_slot[i];
+    st[0] = s0;
+    st[1] = s1;
+    st[2] = s2;
+    st[3] = s3;
 }
 
 // ---------------------------------------------------------------------------

@@ -748,14 +748,40 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         __syncwarp();
         LABS_PHASE(ph_apply)
         const bool hit = step && energy < P.e_l;
-        if (sg.uni(hit)) {
-            unsigned long long slot = 0;
-            if (hit && sl == 0) slot = atomicAdd(P.rec_count, 1ull);
-            slot = sg.bcast(slot);
+        if (sg.uni(hit)) {  // K2: warp-aggregated compaction into the record ring
+            // one atomicAdd per warp for the hits of all its segments: the segment leaders'
+            // ballot gives the count and each segment's rank
+            const uint32_t lead = __ballot_sync(FULLMASK, hit && sl == 0);
+            const int first = __ffs(lead) - 1;
+            unsigned long long base = 0;
+            if (sg.lane == first) base = atomicAdd(P.rec_count, (unsigned long long)__popc(lead));
+            base = __shfl_sync(FULLMASK, base, first);
+            const unsigned long long slot =
+                base + (unsigned long long)__popc(lead & ((1u << sg.base) - 1u));
+            // a slot past the ring's first lap waits until the host has drained everything up
+            // to slot - rec_cap (rec_tail).  The wait loop exits on a warp vote, so the walk
+            // loop stays provably converged; after kRingWaitSpins sleeps of ~4 us (~20 s) it
+            // gives up and raises ctl[0] (the host fails the call instead of hanging).
+            bool wait = hit && slot >= (unsigned long long)P.rec_cap;
+            bool wrote = hit;
+            unsigned spins = 0;
+            while (__any_sync(FULLMASK, wait)) {
+                if (wait) {
+                    const unsigned long long tail = *(volatile const unsigned long long*)P.rec_tail;
+                    if (slot < tail + (unsigned long long)P.rec_cap) {
+                        wait = false;
+                    } else if (++spins >= kRingWaitSpins) {
+                        P.ctl[0] = 1;
+                        wait = wrote = false;
+                    }
+                }
+                __nanosleep(4000);
+            }
             if (hit) {
                 ++emitted;
-                if ((long long)slot < P.rec_cap) {
-                    uint32_t* r = P.rec + slot * (unsigned long long)P.rec_words;
+                if (wrote) {
+                    uint32_t* r = P.rec + (slot & (unsigned long long)(P.rec_cap - 1)) *
+                                              (unsigned long long)P.rec_words;
                     if (sl == 0) {
                         r[0] = (uint32_t)walk;
                         r[1] = (uint32_t)(it + 1);
@@ -765,8 +791,12 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                         r[5] = (uint32_t)(hf >> 32);
                     }
                     for (int i = sl; i < P.hw; i += LPW) r[kRecHeader + i] = w.half[i];
+                    __threadfence();  // each writer's record words before the tag
                 }
             }
+            __syncwarp();
+            if (wrote && sl == 0)
+                P.rec_tag[slot & (unsigned long long)(P.rec_cap - 1)] = (uint32_t)(P.rec_seq0 + slot + 1);
         }
     }
 #ifdef LABS_PHASE_CLOCKS
@@ -838,6 +868,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
     const int64_t nwarps = (int64_t)gridDim.x * P.warps_per_block;
     int64_t grp = (int64_t)blockIdx.x * P.warps_per_block + warp;
     while (grp * SEGS < P.nwalks) {
+        if (*(volatile int*)&P.ctl[1]) break;  // cancelled by the host (pool stopped)
         const int64_t walk = grp * SEGS + seg;
         run_walk_seg<R, LPW, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, walk < P.nwalks,
                                     sg, score_out, corr_out);
