@@ -252,8 +252,94 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     return "";
 }
 
+// K1t geometry (saw_walk_mma.cuh): one walk per warp, 16-row q-tiles covering half indices
+// a in [2 b0, 2 b0 + 256 nq), b0 = p/2; parity arrays with three byte-shifted copies; the
+// kernel's byte offset of d = 0 stays 3 mod 4 (K1's lag-word stores) and kdelta aligns the
+// A fragments instead.
+static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
+                                        uint64_t bloom_bits, int bloom_k, WalkParams& wp) {
+    wp = WalkParams{};
+    wp.kernel = 1;
+    wp.L = L;
+    wp.k = (L - 1) / 2;
+    wp.kp1 = wp.k + 1;
+    wp.p = p;
+    wp.lpw = 32;
+    const int b0 = p >> 1;
+    wp.nq = (wp.k - 2 * b0) / 256 + 1;  // k <= 2 b0 + 256 nq - 1
+    if (wp.nq > 2) return "saw: K1t covers at most 512 half positions";
+    wp.R = 8 * wp.nq;
+    wp.S = std::max(1, (wp.k + 3) / 4);
+    if ((wp.S + 31) / 32 > std::min(4, (256 * wp.nq + 64 + 127) / 128))
+        return "saw: K1t lag words exceed the lane budget";
+    wp.nwx = (wp.kp1 + 3) / 4;
+    wp.kdelta = ((3 - b0 - 7) % 4 + 4) % 4;       // (koff - D) == 0 mod 4, koff == 3 mod 4
+    const int D = b0 + 7 + wp.kdelta;
+    wp.nks = round_up((wp.kp1 + 7 + wp.kdelta + 31) / 32, 2);  // (even: g_mma's unroll)
+    // X: front reads down to -(k + 8) (T update, C update), B reads from -10; back reads up to
+    // k/2 + 4S + 12 (C update), 4 (nwx + S + 3) (correlation init), 32 nks + 16 (B) and
+    // 1.5 k + 4 (T update)
+    wp.xoff = 4 * round_up(std::max(wp.S + 2, (wp.k + 12) / 4 + 1), 2);
+    const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3),
+                              32 * wp.nks + 24, wp.k + wp.k / 2 + 8});
+    wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
+    // K: A reads d from -(128 nq + D + 4) to 32 nks - D + 4; lag-word stores |d| <= 4S + 4
+    int koff = std::max(128 * wp.nq + D + 16, 4 * wp.S + 12);
+    while (koff % 4 != 3) ++koff;
+    wp.koff = koff;
+    wp.kwords = round_up((koff + std::max(32 * wp.nks + 16, 4 * wp.S + 16)) / 4, 4);
+    wp.hw = (wp.kp1 + 31) / 32;
+    if (bloom_bits >= (1ull << 32)) return "saw: Bloom filter exceeds 2^32 bits";
+    if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";
+    wp.bloom_bits = static_cast<uint32_t>(bloom_bits);
+    wp.bloom_k = bloom_k;
+    wp.bloom_words = round_up(static_cast<int>((bloom_bits + 31) / 32), 4);
+    wp.bloom_mu = static_cast<uint64_t>((static_cast<unsigned __int128>(1) << 64) / bloom_bits);
+    wp.t_i = t_i;
+    wp.e_l = e_l;
+    int x1 = wp.xwords;
+    while (x1 % 32 != 16) x1 += 4;
+    wp.off_x1 = x1;
+    wp.off_xc = wp.off_x1 + wp.xwords;
+    wp.off_kl = wp.off_xc + 6 * wp.xwords;
+    wp.off_kh = wp.off_kl + wp.kwords;
+    wp.off_half = wp.off_kh + wp.kwords;
+    wp.off_dc = wp.off_half;
+    wp.off_bloom = wp.off_half + round_up(wp.hw, 4);
+    wp.off_c16 = wp.off_bloom;
+    wp.off_kq = wp.off_c16 + 2 * round_up(wp.S, 4);
+    const int init_words = 2 * round_up(wp.S, 4) + round_up(wp.kp1, 4);
+    wp.warp_words = wp.off_bloom + std::max(wp.bloom_words, init_words);
+    if (wp.warp_words % 8 == 0) wp.warp_words += 4;
+    wp.fm_words = 0;
+    int wpb = 4;
+    while (wpb > 1 && wpb * wp.warp_words * 4 > 227 * 1024) --wpb;
+    if (wpb * wp.warp_words * 4 > 227 * 1024)
+        return "saw: per-walk state (Bloom filter) exceeds shared memory; lower T_i or raise "
+               "--bloom-fpr";
+    wp.warps_per_block = wpb;
+    wp.walks_per_block = wpb;
+    wp.rec_words = kRecHeader + wp.hw;
+    return "";
+}
+
+// Which walk kernel: K1t (tensor-core G) from kMmaMinFree free half positions on, K1
+// below (LABS_KERNEL=dp4a|mma forces one: A/B timing, tests).
+static constexpr int kMmaMinFree = 200;
+
 std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bloom_bits,
                              int bloom_k, WalkParams& wp) {
+    const char* kern = std::getenv("LABS_KERNEL");
+    const int free_bits = (L + 1) / 2 - p;
+    const int k = (L - 1) / 2;
+    const bool fits_mma = k - 2 * (p >> 1) < 512 && std::getenv("LABS_LPW") == nullptr;
+    bool mma = fits_mma && free_bits >= kMmaMinFree;
+    if (kern && std::string(kern) == "mma") mma = fits_mma;
+    if (kern && std::string(kern) == "dp4a") mma = false;
+    if (mma) {
+        std::string err = make_walk_params_mma(L, p, t_i, e_l, bloom_bits, bloom_k, wp);
+        if (err.empty()) return err;
+    }
     return make_walk_params_impl(L, p, t_i, e_l, bloom_bits, bloom_k, wp, 0);
 }
 

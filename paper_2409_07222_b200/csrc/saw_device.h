@@ -41,6 +41,12 @@ struct WalkParams {
     int32_t debug_check;           // re-derive E from C every iteration, flag divergence
     int32_t count_visited;         // full Bloom probes of every free neighbour (exact stats)
     int32_t rec_words;             // kRecHeader + hw
+    // K1t (tensor-core G, saw_walk_mma.cuh): kernel = 1
+    int32_t kernel;                // 0 = K1 (IDP4A G), 1 = K1t (mma.sync s8 G)
+    int32_t nq;                    // K1t: 16-row q-tiles per parity (neighbours 256 nq)
+    int32_t nks;                   // K1t: 32-deep k-steps
+    int32_t kdelta;                // K1t: D = p/2 + 7 + kdelta aligns the kernel words
+    int32_t off_xc;                // K1t: three byte-shifted copies per parity array
     int64_t nwalks;                // walks in this launch
     int64_t rec_cap;               // record ring slots (a power of two)
     // inputs (device pointers)

@@ -7,6 +7,14 @@
 #include "saw_walk.h"
 
 namespace labs_b200 {
+template <int NQ>
+cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
+                            int* score_out, int* corr_out, bool count);
+template <int NQ>
+int blocks_per_sm_mma(const WalkParams& P, size_t smem);
+}  // namespace labs_b200
+
+namespace labs_b200 {
 
 // ---------------------------------------------------------------------------
 // K3: one thread per segment (restarts [r0, r1) of one walker), drawn in order from the
@@ -82,6 +90,9 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
                             int* corr_out) {
     const size_t smem = walk_smem_bytes(P);
     const bool count = P.count_visited != 0;
+    if (P.kernel == 1)
+        return P.nq == 1 ? launch_walk_mma<1>(P, grid, smem, st, score_out, corr_out, count)
+                         : launch_walk_mma<2>(P, grid, smem, st, score_out, corr_out, count);
     switch (P.R * (P.lpw == 16 ? -1 : 1) + (P.lpw == 8 ? 1000 : 0)) {
 #define LABS_CASE(r)                                                                   \
     case r: return launch_walk_fixed<r, 32>(P, grid, smem, st, score_out, corr_out, count); \
@@ -97,6 +108,7 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
 
 static int walk_blocks_for(const WalkParams& P) {
     const size_t smem = walk_smem_bytes(P);
+    if (P.kernel == 1) return P.nq == 1 ? blocks_per_sm_mma<1>(P, smem) : blocks_per_sm_mma<2>(P, smem);
     switch (P.R * (P.lpw == 16 ? -1 : 1) + (P.lpw == 8 ? 1000 : 0)) {
 #define LABS_CASE(r)                                 \
     case r: return blocks_per_sm_fixed<r, 32>(P, smem); \

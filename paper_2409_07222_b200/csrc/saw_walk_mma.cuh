@@ -1,0 +1,674 @@
+// saw_walk_mma.cuh -- K1t, the tensor-core variant of the Step-1 walk kernel (sm_100a).
+//
+// Same walk as K1 (saw_walk.cuh: run_walk, saw.cpp:117-149, with the fused Bloom probe,
+// skew flip-delta argmin, apply and sieve), one walk per warp, but the O(L) part of every
+// flip delta -- the sliding dot product G(a) of the parity array with the symmetric
+// correlation kernel K[d] = C_{2|d|} -- runs on the int8 tensor cores as
+// mma.sync.m16n8k32.s8 instead of IDP4A.
+//
+// G as a GEMM.  For neighbour a = 2a' + par, a' = b0 + 8q + r (b0 = p/2, q = 0..15 per
+// q-tile, r = 0..7):
+//     G(a) = sum_d K[d] X_par[a' + d] = sum_kk A[q][kk] B_par[kk][r]
+//     A[q][kk]     = K[kk - 8q - D]         (16 x 32 per k-step: the correlation kernel,
+//                                            row q shifted by 8q bytes -- aligned words)
+//     B_par[kk][r] = X_par[b0 + r + kk - D]  (32 x 8: the parity array, column r shifted
+//                                            by r bytes -- read from 4 byte-shifted copies
+//                                            of X_par so every fragment word is aligned)
+// with D = b0 + 7 + delta (delta aligns A to words).  A is shared by both parities, so a
+// k-step is two MMAs (one per parity) per q-tile; nks = ceil((k+1+7+delta)/32) k-steps
+// cover every nonzero product.  The accumulator fragment gives lane (g, t) the neighbours
+// a = A0 + {0, 2, 128, 130} (par 0) and A0 + {1, 3, 129, 131} (par 1), A0 = 2 b0 + 16 g + 4 t
+// (+256 per q-tile).  Products are int8 x {-1, 0, 1} accumulated in int32: exact.  While
+// some |C| > 127 a second pass runs on the high bytes (G = 256 G_hi + G_lo), as in K1.
+//
+// The rest of the step (key-scaled T registers, lexicographic argmin by REDUX, lazy Bloom
+// probe, even-lag C update by one-hot IDP4A, hashes, sieve + K2 ring compaction) is K1's
+// bookkeeping at 32 lanes per walk; DESIGN.md §4 has the instruction budget.
+#pragma once
+#include "saw_walk.cuh"
+
+namespace labs_b200 {
+
+__device__ __forceinline__ void mma_s8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Per-walk shared-memory views of K1t (offsets: make_walk_params, kernel 1).  Pointers are
+// computed from (parity, copy) arithmetically: an indexed pointer table would live in local
+// memory.
+struct MmaSmem {
+    uint32_t* base;
+    int off_x1, off_xc, xwords;
+    uint32_t* KL;        // correlation kernel, low / high bytes (byte koff + d = C_{2|d|})
+    uint32_t* KH;
+    uint32_t* C16;       // (initialisation only, inside the Bloom words)
+    int* KQ;
+    uint32_t* half;
+    uint32_t* bloom;
+    __device__ __forceinline__ uint32_t* Xw(int par) const { return base + par * off_x1; }
+    __device__ __forceinline__ int8_t* X(int par) const { return reinterpret_cast<int8_t*>(Xw(par)); }
+    // copy c of parity par: byte j = X(par) byte j + c (copy 0 is X(par) itself)
+    __device__ __forceinline__ uint32_t* Xc(int par, int c) const {
+        return c == 0 ? Xw(par) : base + off_xc + (par * 3 + c - 1) * xwords;
+    }
+};
+
+// neighbour slot m of a lane: a = A0 + kOff8[m % 8] + 256 (m / 8); accumulator element
+// kOff8 order: par 0 d0..d3, par 1 d0..d3
+__device__ __forceinline__ constexpr int mma_off(int m) {
+    return (m / 8) * 256 + ((m & 4) ? 1 : 0) + ((m & 1) ? 2 : 0) + ((m & 2) ? 128 : 0);
+}
+
+// G of this lane's 8 NQ neighbours: acc[jq][par][i] (i = accumulator element).  nks is even
+// (make_walk_params pads with zero k-steps).  The A fragment of k-step s is {a0(s), a0(s-2),
+// a2(s), a2(s-2)} (rows g+8 sit 64 bytes = two k-steps lower), so each step loads two kernel
+// words and reuses two; even and odd steps accumulate in separate chains.
+template <int NQ>
+__device__ __forceinline__ void g_mma(const uint32_t* __restrict__ Kw, int nks, int kidx0, int xb,
+                                      const uint32_t* __restrict__ xc0,
+                                      const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
+    int ac2[NQ][2][4];
+    uint32_t p0[NQ][2], p2[NQ][2];  // a0, a2 of steps s - 2 (h = 0) and s - 1 (h = 1)
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+        const int ki = kidx0 - 32 * j;
+        p0[j][0] = Kw[ki - 16];
+        p2[j][0] = Kw[ki - 12];
+        p0[j][1] = Kw[ki - 8];
+        p2[j][1] = Kw[ki - 4];
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ac2[j][p][i] = 0;
+    }
+    const uint32_t* kp = Kw + kidx0;
+    const uint32_t* x0 = xc0 + xb;
+    const uint32_t* x1 = xc1 + xb;
+    const uint32_t* const kend = kp + 8 * nks;
+#pragma unroll 1
+    for (; kp != kend; kp += 16, x0 += 16, x1 += 16) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t b00 = x0[8 * h], b01 = x0[8 * h + 4];
+            const uint32_t b10 = x1[8 * h], b11 = x1[8 * h + 4];
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+                const uint32_t c0 = kp[8 * h - 32 * j], c2 = kp[8 * h - 32 * j + 4];
+                const uint32_t a[4] = {c0, p0[j][h], c2, p2[j][h]};
+                p0[j][h] = c0;
+                p2[j][h] = c2;
+                if (h == 0) {
+                    mma_s8(acc[j][0], a, b00, b01);
+                    mma_s8(acc[j][1], a, b10, b11);
+                } else {
+                    mma_s8(ac2[j][0], a, b00, b01);
+                    mma_s8(ac2[j][1], a, b10, b11);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][p][i] += ac2[j][p][i];
+}
+
+template <int NQ, bool COUNT>
+__device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64_t* fm0,
+                             const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
+                             int* score_out, int* corr_out) {
+    constexpr int LPW = 32;
+    constexpr int R = 8 * NQ;
+    // lag words a lane owns: S = ceil(k/4) <= (2 b0 + 256 NQ + 3) / 4 with b0 <= 15
+    constexpr int NJ = (256 * NQ + 64 + 127) / 128 < 4 ? (256 * NQ + 64 + 127) / 128 : 4;
+    const Seg<LPW> sg(threadIdx.x & 31);
+    const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
+    const int sl = sg.sl;
+    const int nj = (S + LPW - 1) / LPW;
+
+    // ---- load the initial half, build parity arrays + their byte-shifted copies ----
+    const uint32_t* src = P.halves + (valid ? walk : 0) * P.hw;
+    for (int i = sl; i < P.hw; i += LPW) w.half[i] = valid ? src[i] : 0u;
+    __syncwarp();
+    for (int wi = sl; wi < 2 * P.xwords; wi += LPW) {
+        const int par = wi >= P.xwords;
+        const int word = wi - par * P.xwords;
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int li = word * 4 + b - P.xoff;
+            const int j = 2 * li + par;
+            const int x = (li >= 0 && j < L) ? x_of_half(w.half, k, j) : 0;
+            v |= ((uint32_t)x & 0xffu) << (8 * b);
+        }
+        w.Xw(par)[word] = v;
+    }
+    for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
+    __syncwarp();
+    for (int wi = sl; wi < 6 * P.xwords; wi += LPW) {  // copies c = 1..3 of both parities
+        const int par = wi / (3 * P.xwords);
+        const int rem = wi - par * 3 * P.xwords;
+        const int c = 1 + rem / P.xwords;
+        const int word = rem - (c - 1) * P.xwords;
+        const uint32_t lo = w.Xw(par)[word];
+        const uint32_t hi = word + 1 < P.xwords ? w.Xw(par)[word + 1] : 0u;
+        w.Xc(par, c)[word] = prmt(lo, hi, sel4(c));
+    }
+
+    // ---- exact C_{2t} of the owned lag words (registers), E, max|C| ----
+    WarpSmem ws{};  // (views the K1 helpers expect)
+    ws.X0 = w.X(0);
+    ws.X1 = w.X(1);
+    ws.X0w = w.Xw(0);
+    ws.X1w = w.Xw(1);
+    ws.KL = w.KL;
+    ws.KH = w.KH;
+    ws.C16 = w.C16;
+    ws.KQ = w.KQ;
+    ws.half = w.half;
+    ws.bloom = w.bloom;
+    int e_part = 0, cmax = 0;
+    int C[NJ][4];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) {
+        const int s = sl + LPW * jj;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int t = 4 * s + 1 + b;
+            int v = 0;
+            if (jj < nj && s < S && t <= k) v = corr_even_lag(ws, P, t);
+            C[jj][b] = v;
+            e_part += v * v;
+            cmax = max(cmax, abs(v));
+        }
+    }
+    int energy = sg.sum(e_part);
+    bool wide = sg.any(cmax > 127);
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) {
+        const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1, LPW);
+        const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
+        const int s = sl + LPW * jj;
+        const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
+        if (jj < nj && s < S) {
+            store_c_word(ws, P, s, C[jj], cprev, wide);
+            if (corr_out && valid)
+                for (int b = 0; b < 4; ++b)
+                    if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = C[jj][b];
+        }
+    }
+
+    // ---- 16N + 32Q per half index (lanes over a), once per walk ----
+    for (int a = P.p + sl; a <= k; a += LPW) {
+        const int8_t* Xb = w.X(a & 1) + P.xoff + (a >> 1);
+        const int tstar = (a < k) ? (k - a) : -1;
+        int q = 0;
+        for (int t = 1; 2 * t <= a; ++t)
+            if (t != tstar) q += (int)Xb[-t] * (int)Xb[t];
+        const int n = (a >> 1) + ((L - 1 - a) >> 1) - (a < k ? 1 : 0);
+        w.KQ[a] = (a < k) ? 16 * n + 32 * q : 4 * n + 8 * q;
+    }
+    __syncwarp();
+
+    // ---- lane geometry (the accumulator fragment layout) ----
+    const int lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+    const int b0 = P.p >> 1;
+    const int A0 = 2 * b0 + 16 * gq + 4 * tq;
+    // A (kernel) word of k-step 0, q-tile 0, row gq, columns 4tq..4tq+3
+    const int D = b0 + 7 + P.kdelta;
+    const int kidx0 = (P.koff - D) / 4 + tq - 2 * gq;
+    // B (parity) words: byte xoff + gq + 4tq - 7 - delta of X_par, from copy c
+    const int jb = P.xoff + gq + 4 * tq - 7 - P.kdelta;
+    const int cb = jb & 3;
+    const int xb = (jb - cb) >> 2;
+    const uint32_t* xc0 = w.Xc(0, cb);
+    const uint32_t* xc1 = w.Xc(1, cb);
+    const bool one_key = L <= 1001;
+    const bool dbg = P.debug_check != 0;
+    const int sc = one_key ? 512 : 1;
+    uint32_t T[R];
+    int xs[R];
+    uint32_t inval = 0;
+    {
+        const int16_t* C16h = reinterpret_cast<const int16_t*>(w.C16);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int a = A0 + mma_off(m);
+            int t = 0;
+            xs[m] = 0;
+            if (a < P.p || a > k) {
+                inval |= 1u << m;
+            } else if (a < k) {
+                const int sgn8 = ((k - a) & 1) ? -8 : 8;
+                t = w.KQ[a] + sgn8 * (int)C16h[k - a - 1];
+                xs[m] = 8 * (int)w.X(a & 1)[P.xoff + (a >> 1)];
+            } else {
+                t = w.KQ[a];
+                xs[m] = 4 * (int)w.X(a & 1)[P.xoff + (a >> 1)];
+            }
+            T[m] = (uint32_t)(t * sc) + (one_key ? 0x80000000u + (uint32_t)a : 0u);
+            xs[m] *= -sc;
+        }
+    }
+
+    // ---- clear the Bloom filter (it held C16 and KQ until here) ----
+    __syncwarp();
+    {
+        uint4* b4 = reinterpret_cast<uint4*>(w.bloom);
+        for (int i = sl; i < (P.bloom_words >> 2); i += LPW) b4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
+    // ---- half hashes h1, h2 (saw.cpp:77-89), dedup hash, initial Bloom insert ----
+    uint64_t h1 = 0, h2 = 0;
+    for (int i = sl; i < kp1; i += LPW) {
+        const int bit = (w.half[i >> 5] >> (i & 31)) & 1;
+        h1 ^= P.tab[(0 * kp1 + i) * 2 + bit];
+        h2 ^= P.tab[(1 * kp1 + i) * 2 + bit];
+    }
+    h1 = sg.xor64(h1) ^ P.salt0;
+    h2 = sg.xor64(h2) ^ P.salt1;
+    uint64_t hf = 0;
+    for (int j = sl; j < L; j += LPW) hf ^= P.tabfull[2 * j + (x_of_half(w.half, k, j) > 0)];
+    hf = sg.xor64(hf) ^ P.salt_full;
+    for (int i = sl; i < P.bloom_k; i += LPW) {
+        const uint32_t idx = bloom_index(h1, h2, i, P.bloom_mu, P.bloom_bits);
+        atomicOr(&w.bloom[idx >> 5], 1u << (idx & 31));
+    }
+    __syncwarp();
+
+    const int e0 = energy;
+    int best = energy;
+    int iterations = 0, emitted = 0, wide_iters = 0, diverged = 0;
+    long long probes = 0;
+    long long evals_part = 0;
+    int exhausted = 0;
+    uint32_t skip = inval;
+    const int t_i32 = score_out ? 1 : (int)P.t_i;
+    bool active = valid;
+
+    for (int it = 0;; ++it) {
+        const bool cont = active && it < t_i32;
+        if (!cont) break;  // (one walk per warp: warp-uniform)
+        // ---- G for all neighbours on the tensor cores ----
+        int acc[NQ][2][4];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j)
+#pragma unroll
+            for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][p2][i] = 0;
+        if (wide) {  // G = 256 G_high + G_low
+            g_mma<NQ>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
+#pragma unroll
+            for (int j = 0; j < NQ; ++j)
+#pragma unroll
+                for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][p2][i] *= 256;
+            ++wide_iters;
+        }
+        g_mma<NQ>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
+        // ---- exact deltas / keys: dE(a) = T(a) - xs(a) G(a) ----
+        int delta[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int gv = acc[m / 8][(m >> 2) & 1][m & 3];
+            delta[m] = (int)(T[m] + (uint32_t)xs[m] * (uint32_t)gv);
+        }
+        if (score_out) {
+            if (valid)
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const int a = A0 + mma_off(m);
+                    if (!(inval & (1u << m)))
+                        score_out[walk * kp1 + a] =
+                            one_key ? (int)((uint32_t)delta[m] - 0x80000000u - (uint32_t)a) >> 9 : delta[m];
+                }
+            break;
+        }
+
+        // ---- choose: lowest (delta, hp) among unvisited (best_neighbour, saw.cpp:106-115) ----
+        if (COUNT) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (inval & (1u << m)) continue;
+                const int a = A0 + mma_off(m);
+                const uint64_t n1 = h1 ^ fm0[a], n2 = h2 ^ fm1[a];
+                bool hit = true;
+                for (int i = 0; i < P.bloom_k; ++i) {
+                    const uint32_t idx = bloom_index(n1, n2, i, P.bloom_mu, P.bloom_bits);
+                    if (!((w.bloom[idx >> 5] >> (idx & 31)) & 1)) {
+                        hit = false;
+                        break;
+                    }
+                }
+                if (hit) skip |= 1u << m;
+                else ++evals_part;
+            }
+        }
+        int dstar = 0, astar = -1;
+        uint32_t ins_idx = 0;
+        uint32_t bkey = 0xffffffffu;
+        int bd = INT_BIG, bm = 0;
+        if (one_key) {
+            bkey = lane_min_key<R>(delta, skip);
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                if (!(skip & (1u << m)) && delta[m] < bd) {
+                    bd = delta[m];
+                    bm = m;
+                }
+        }
+        for (;;) {
+            int md, ma;
+            bool mine_won;
+            if (one_key) {
+                const uint32_t k_best = __reduce_min_sync(FULLMASK, bkey);
+                if (k_best == 0xffffffffu) break;  // every free neighbour visited
+                ma = (int)(k_best & 511u);
+                md = (int)(k_best >> 9) - (1 << 22);
+                mine_won = bkey == k_best;
+            } else {
+                md = __reduce_min_sync(FULLMASK, bd);
+                if (md == INT_BIG) break;
+                const int mine = (bd == md) ? A0 + mma_off(bm) : INT_BIG;
+                ma = __reduce_min_sync(FULLMASK, mine);
+                mine_won = mine == ma;
+            }
+            bool bit = true;
+            if (sl < P.bloom_k) {
+                const uint32_t idx = bloom_index(h1 ^ fm0[ma], h2 ^ fm1[ma], sl, P.bloom_mu, P.bloom_bits);
+                bit = (w.bloom[idx >> 5] >> (idx & 31)) & 1;
+                ins_idx = idx;
+            }
+            if (COUNT) {
+                dstar = md;
+                astar = ma;
+                break;
+            }
+            const bool visited = __all_sync(FULLMASK, bit);
+            ++probes;
+            if (!visited) {
+                dstar = md;
+                astar = ma;
+                break;
+            }
+            if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
+                const int d = ma - A0;
+                const int mm = (d >> 8) * 8 + (d & 1) * 4 + (((d & 255) >> 7) << 1) + ((d >> 1) & 1);
+                skip |= 1u << mm;
+                if (one_key) {
+                    bkey = lane_min_key<R>(delta, skip);
+                } else {
+                    bd = INT_BIG;
+                    bm = 0;
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        if (!(skip & (1u << m)) && delta[m] < bd) {
+                            bd = delta[m];
+                            bm = m;
+                        }
+                }
+            }
+        }
+        if (astar < 0) {
+            exhausted = 1;
+            active = false;
+            break;
+        }
+
+        // ---- apply the skew flip at astar (apply_skew_flip, skew.cpp:95-105) ----
+        ++iterations;
+        const int as = astar;
+        const bool cen = as == k;
+        const int bstar = L - 1 - as;
+        const int apar = as & 1, ah = as >> 1;
+        int8_t* Xa = w.X(apar) + P.xoff;
+        const int xa = Xa[ah];
+        const int xb = cen ? 0 : (((k - as) & 1) ? -xa : xa);
+        h1 ^= fm0[as];
+        h2 ^= fm1[as];
+        hf ^= fmf[as];
+        if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
+        energy += dstar;
+        best = min(best, energy);
+        // (1) zero x_a and x_b in the primary array (the T and C updates read the fused
+        //     rule's pre-step sequence from it; the MMA copies are rewritten in (4))
+        __syncwarp();
+        if (sl == 0) Xa[ah] = 0;
+        if (sl == 1) Xa[bstar >> 1] = 0;
+        __syncwarp();
+        // (2) T updates from the zeroed pre-step sequence (K1's rules), four neighbours a = A + e
+        //     (e = 0..3) per group at once.  Byte e of three windows holds f_a = x_{a*+2(k-a)},
+        //     g_a = x_{a*-2(k-a)} (= x_{2a-b*}) and p_a = x_{2a-a*}; one-hot int8 selectors carry
+        //     the coefficients, so a neighbour costs three IDP4A and one IMAD:
+        //       T(a) += 8 sc [ c_a (f_a + g_a) - 8 x_a* p_a - 8 x_b* g_a ],  c_a = (-1)^(k-a) mul
+        //     (the Q terms only for a of a*'s parity; the pair excluded from Q(a) and the undo
+        //     move's own Q term are taken back in the rare fix-up below).
+        const int mul = cen ? -2 * xa : -4 * xa;
+        {
+            const int c0 = (k & 1) ? -mul : mul;  // c_a for e = 0 (A is even); alternates with e
+            uint32_t sf[4], sg[4], sx[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ce = (e & 1) ? -c0 : c0;
+                const bool same = (e & 1) == apar;
+                sf[e] = ((uint32_t)ce & 0xffu) << (8 * e);
+                sg[e] = ((uint32_t)(ce - (same ? 8 * xb : 0)) & 0xffu) << (8 * e);
+                sx[e] = same ? ((uint32_t)(-8 * xa) & 0xffu) << (8 * e) : 0u;
+            }
+            const uint32_t* Xaw = w.Xw(apar);
+            const int sc8 = 8 * sc;
+#pragma unroll
+            for (int grp = 0; grp < 2 * NQ; ++grp) {
+                const int Aa = min(A0 + 128 * grp, k);  // (addresses of invalid groups stay in range)
+                const int bf = P.xoff + ah + k - Aa - 3, bg = P.xoff + ah - k + Aa,
+                          bx = P.xoff + Aa - ah - apar;
+                const uint32_t wf = prmt(Xaw[bf >> 2], Xaw[(bf >> 2) + 1], sel4r(bf & 3));
+                const uint32_t wg = prmt(Xaw[bg >> 2], Xaw[(bg >> 2) + 1], sel4(bg & 3));
+                const uint32_t wx = prmt(Xaw[bx >> 2], Xaw[(bx >> 2) + 1], sel4(bx & 3));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
+                    const int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e],
+                                                                     __dp4a((int)wx, (int)sx[e], 0)));
+                    T[m] += (uint32_t)(v * sc8);
+                }
+            }
+            // fix-ups: a = a* (undo move: its Q term through b* is excluded, xs flips, it is
+            // skipped next step) and a with 3a = a* + L - 1 (its Q pair through a* is excluded)
+            const int down = as - A0;
+            const int ex3 = as + L - 1;
+            const int aex = ex3 / 3;
+            const int dex = (ex3 % 3 == 0 && (aex & 1) == apar && aex >= P.p && aex <= k) ? aex - A0 : -1;
+            const bool own_mine = down >= 0 && (down & 255) < 132 && ((down & 255) < 4 || (down & 255) >= 128) &&
+                                  (down >> 8) < NQ;
+            const bool ex_mine = dex >= 0 && (dex & 255) < 132 && ((dex & 255) < 4 || (dex & 255) >= 128) &&
+                                 (dex >> 8) < NQ;
+            const uint32_t obit = own_mine ? 1u << ((down >> 8) * 8 + (down & 1) * 4 + (((down & 255) >> 7) << 1) + ((down >> 1) & 1)) : 0u;
+            const uint32_t xbit = ex_mine ? 1u << ((dex >> 8) * 8 + (dex & 1) * 4 + (((dex & 255) >> 7) << 1) + ((dex >> 1) & 1)) : 0u;
+            skip = inval | obit;  // the undo move (the previous pivot is in the filter)
+            if ((obit | xbit) & ~inval) {
+                const int vo = 64 * sc * xb * (int)Xa[ah - (k - as)];
+                const int vx = ex_mine ? 64 * sc * xa * (int)Xa[(2 * aex - as) >> 1] : 0;
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const int om = (obit >> m) & 1;
+                    T[m] += (uint32_t)(om * vo + ((xbit >> m) & 1) * vx);
+                    xs[m] = (xs[m] ^ -om) + om;
+                }
+            }
+        }
+        // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
+        int cmx = 0, esp = 0;
+        {
+            const uint32_t* Xaw = w.Xw(apar);
+            const int awF = (P.xoff + ah + 1) >> 2;
+            const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
+            const int awB = (P.xoff + ah - 4) >> 2;
+            const uint32_t asB = sel4r((P.xoff + ah) & 3);
+            const uint32_t mb = (uint32_t)mul & 0xffu;
+            int e1h[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) e1h[b] = (int)prmt(mb, 0u, 0x4444u ^ (0x4u << (4 * b)));
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int s = sl + LPW * jj;
+                if (jj < nj && s < S) {
+                    const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
+                    const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        C[jj][b] = __dp4a((int)fw, e1h[b], __dp4a((int)bw, e1h[b], C[jj][b]));
+                    cmx |= ((C[jj][0] + 128) | (C[jj][1] + 128)) | ((C[jj][2] + 128) | (C[jj][3] + 128));
+                }
+            }
+        }
+        const bool wide_next = __any_sync(FULLMASK, (cmx & ~0xff) != 0);
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int up = __shfl_up_sync(FULLMASK, C[jj][3], 1, LPW);
+            const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
+            const int s = sl + LPW * jj;
+            const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
+            if (jj < nj && s < S) store_k_word(ws, P, s, C[jj], cprev, wide_next);
+        }
+        wide = wide_next;
+        __syncwarp();
+        // (4) write the flipped pair into the primary array and its three shifted copies
+        //     (lanes 0-3: x_a* in copy 0-3, lanes 4-7: x_b*), toggle the half bit (lane 8)
+        if (sl < 8 && !(cen && sl >= 4)) {
+            const int c = sl & 3;
+            const int pos = P.xoff + ((sl < 4) ? ah : (bstar >> 1)) - c;
+            reinterpret_cast<int8_t*>(w.Xc(apar, c))[pos] = (int8_t)((sl < 4) ? -xa : -xb);
+        }
+        if (sl == 8) w.half[as >> 5] ^= 1u << (as & 31);
+        if (dbg) {
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj)
+                if (jj < nj && sl + LPW * jj < S)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) esp += C[jj][b] * C[jj][b];
+            if (sg.sum(esp) != energy) ++diverged;
+        }
+        __syncwarp();
+        if (energy < P.e_l) {  // K2: one ring slot (warp-uniform: one walk per warp)
+            ++emitted;
+            unsigned long long slot = 0;
+            if (sl == 0) slot = atomicAdd(P.rec_count, 1ull);
+            slot = __shfl_sync(FULLMASK, slot, 0);
+            bool wrote = true;
+            bool wait = slot >= (unsigned long long)P.rec_cap;
+            unsigned spins = 0;
+            while (wait) {  // (uniform: every lane evaluates the same slot and tail)
+                const unsigned long long tail = *(volatile const unsigned long long*)P.rec_tail;
+                if (slot < tail + (unsigned long long)P.rec_cap) {
+                    wait = false;
+                } else if (++spins >= kRingWaitSpins) {
+                    if (sl == 0) P.ctl[0] = 1;
+                    wait = wrote = false;
+                } else {
+                    __nanosleep(4000);
+                }
+                wait = __any_sync(FULLMASK, wait);
+                wrote = __all_sync(FULLMASK, wrote);
+            }
+            if (wrote) {
+                uint32_t* r = P.rec + (slot & (unsigned long long)(P.rec_cap - 1)) *
+                                          (unsigned long long)P.rec_words;
+                if (sl == 0) {
+                    r[0] = (uint32_t)walk;
+                    r[1] = (uint32_t)(it + 1);
+                    r[2] = (uint32_t)energy;
+                    r[3] = 0;
+                    r[4] = (uint32_t)hf;
+                    r[5] = (uint32_t)(hf >> 32);
+                }
+                for (int i = sl; i < P.hw; i += LPW) r[kRecHeader + i] = w.half[i];
+                __threadfence();
+            }
+            __syncwarp();
+            if (wrote && sl == 0)
+                P.rec_tag[slot & (unsigned long long)(P.rec_cap - 1)] = (uint32_t)(P.rec_seq0 + slot + 1);
+        }
+    }
+    if (COUNT) evals_part = sg.sum64(evals_part);
+    if (valid && sl == 0 && P.walk_stats) {
+        int64_t* st = P.walk_stats + walk * kWalkStatWords;
+        st[kWsIterations] = iterations;
+        st[kWsEmitted] = emitted;
+        st[kWsBest] = best;
+        st[kWsInitial] = e0;
+        st[kWsExhausted] = exhausted;
+        st[kWsDeltaEvals] = COUNT ? evals_part : -1;
+        st[kWsVisitedProbes] = probes;
+        st[kWsWideIters] = wide_iters;
+        st[kWsDiverged] = diverged;
+    }
+    __syncwarp();
+}
+
+template <int NQ, bool COUNT>
+__global__ void __launch_bounds__(128, NQ == 1 ? 4 : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
+    extern __shared__ uint4 smem_u4[];
+    const uint64_t* fm = P.fm;
+    if (P.fm_words) {
+        uint64_t* fs = reinterpret_cast<uint64_t*>(smem_u4);
+        for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fs[i] = P.fm[i];
+        __syncthreads();
+        fm = fs;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* base = reinterpret_cast<uint32_t*>(smem_u4) + P.fm_words + warp * P.warp_words;
+    MmaSmem w;
+    w.base = base;
+    w.off_x1 = P.off_x1;
+    w.off_xc = P.off_xc;
+    w.xwords = P.xwords;
+    w.KL = base + P.off_kl;
+    w.KH = base + P.off_kh;
+    w.C16 = base + P.off_c16;
+    w.KQ = reinterpret_cast<int*>(base + P.off_kq);
+    w.half = base + P.off_half;
+    w.bloom = base + P.off_bloom;
+    const int64_t nwarps = (int64_t)gridDim.x * P.warps_per_block;
+    int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp;
+    while (walk < P.nwalks) {
+        if (*(volatile int*)&P.ctl[1]) break;  // cancelled by the host (pool stopped)
+        run_walk_mma<NQ, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, true, score_out, corr_out);
+        unsigned long long nx = 0;
+        if (lane == 0) nx = atomicAdd(P.walk_next, 1ull);
+        walk = nwarps + (int64_t)__shfl_sync(FULLMASK, nx, 0);
+    }
+}
+
+template <int NQ>
+cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
+                            int* score_out, int* corr_out, bool count) {
+    auto kfn = count ? saw_walk_mma_kernel<NQ, true> : saw_walk_mma_kernel<NQ, false>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, P.warps_per_block * 32, smem, st>>>(P, score_out, corr_out);
+    return cudaGetLastError();
+}
+
+template <int NQ>
+int blocks_per_sm_mma(const WalkParams& P, size_t smem) {
+    int n = 0;
+    cudaFuncSetAttribute(saw_walk_mma_kernel<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, saw_walk_mma_kernel<NQ, false>,
+                                                      P.warps_per_block * 32, smem) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+}  // namespace labs_b200
