@@ -455,6 +455,21 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         //     move's own Q term are taken back in the rare fix-up below).
         const int mul = cen ? -2 * xa : -4 * xa;
         {
+            // the two exceptions, each in at most one lane: a = a* (the undo move: its Q term
+            // through b* is excluded, xs flips, it is skipped next step) and a with
+            // 3a = a* + L - 1 (its Q pair through a* is excluded)
+            constexpr int kSlotMask = ~(0x83 | (NQ == 2 ? 0x100 : 0));  // slot offsets: bits 0,1,7(,8)
+            const int down = as - A0;
+            const int ex3 = as + L - 1;
+            const int aex = ex3 / 3;
+            const int dex = (ex3 - 3 * aex == 0 && (aex & 1) == apar && aex >= P.p) ? aex - A0 : -1;
+            const int mo = (down >= 0 && (down & kSlotMask) == 0)
+                               ? (down >> 8) * 8 + (down & 1) * 4 + ((down >> 6) & 2) + ((down >> 1) & 1) : -1;
+            const int mx = (dex >= 0 && (dex & kSlotMask) == 0)
+                               ? (dex >> 8) * 8 + (dex & 1) * 4 + ((dex >> 6) & 2) + ((dex >> 1) & 1) : -1;
+            const int vo = 8 * xb * (int)Xa[ah - (k - as)];      // (unscaled corrections)
+            const int vx = mx >= 0 ? 8 * xa * (int)Xa[(2 * aex - as) >> 1] : 0;
+            skip = inval | (mo >= 0 ? 1u << mo : 0u);
             const int c0 = (k & 1) ? -mul : mul;  // c_a for e = 0 (A is even); alternates with e
             uint32_t sf[4], sg[4], sx[4];
 #pragma unroll
@@ -478,32 +493,14 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
-                    const int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e],
-                                                                     __dp4a((int)wx, (int)sx[e], 0)));
+                    int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e],
+                                                                __dp4a((int)wx, (int)sx[e], 0)));
+                    if (m == mo) {
+                        v += vo;
+                        xs[m] = -xs[m];
+                    }
+                    if (m == mx) v += vx;
                     T[m] += (uint32_t)(v * sc8);
-                }
-            }
-            // fix-ups: a = a* (undo move: its Q term through b* is excluded, xs flips, it is
-            // skipped next step) and a with 3a = a* + L - 1 (its Q pair through a* is excluded)
-            const int down = as - A0;
-            const int ex3 = as + L - 1;
-            const int aex = ex3 / 3;
-            const int dex = (ex3 % 3 == 0 && (aex & 1) == apar && aex >= P.p && aex <= k) ? aex - A0 : -1;
-            const bool own_mine = down >= 0 && (down & 255) < 132 && ((down & 255) < 4 || (down & 255) >= 128) &&
-                                  (down >> 8) < NQ;
-            const bool ex_mine = dex >= 0 && (dex & 255) < 132 && ((dex & 255) < 4 || (dex & 255) >= 128) &&
-                                 (dex >> 8) < NQ;
-            const uint32_t obit = own_mine ? 1u << ((down >> 8) * 8 + (down & 1) * 4 + (((down & 255) >> 7) << 1) + ((down >> 1) & 1)) : 0u;
-            const uint32_t xbit = ex_mine ? 1u << ((dex >> 8) * 8 + (dex & 1) * 4 + (((dex & 255) >> 7) << 1) + ((dex >> 1) & 1)) : 0u;
-            skip = inval | obit;  // the undo move (the previous pivot is in the filter)
-            if ((obit | xbit) & ~inval) {
-                const int vo = 64 * sc * xb * (int)Xa[ah - (k - as)];
-                const int vx = ex_mine ? 64 * sc * xa * (int)Xa[(2 * aex - as) >> 1] : 0;
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    const int om = (obit >> m) & 1;
-                    T[m] += (uint32_t)(om * vo + ((xbit >> m) & 1) * vx);
-                    xs[m] = (xs[m] ^ -om) + om;
                 }
             }
         }
