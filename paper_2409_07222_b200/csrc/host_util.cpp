@@ -300,8 +300,11 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
     int x1 = wp.xwords;
     while (x1 % 32 != 16) x1 += 4;
     wp.off_x1 = x1;
+    // copies cover only the B reads: bytes [xoff - 16, xoff + 32 nks + 32)
+    wp.xcl = wp.xoff - 16;
+    wp.xcw = 8 * wp.nks + 12;
     wp.off_xc = wp.off_x1 + wp.xwords;
-    wp.off_kl = wp.off_xc + 6 * wp.xwords;
+    wp.off_kl = wp.off_xc + 6 * wp.xcw;
     wp.off_kh = wp.off_kl + wp.kwords;
     wp.off_half = wp.off_kh + wp.kwords;
     wp.off_dc = wp.off_half;

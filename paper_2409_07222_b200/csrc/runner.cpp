@@ -13,6 +13,7 @@ cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int*
                             int* corr_out);
 cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st);
 int walk_blocks_per_sm(WalkParams& P);  // (also places the fm table)
+size_t walk_smem_bytes(const WalkParams& P);
 
 namespace {
 constexpr int64_t kDefaultRingSlots = 1 << 16;
@@ -105,6 +106,11 @@ void DeviceRunner::init(int device, const WalkParams& params) {
     const int bps = std::max(1, walk_blocks_per_sm(wp));
     grid_cap = sms * bps;
     resident = static_cast<int64_t>(grid_cap) * wp.walks_per_block;
+    if (std::getenv("LABS_TIMING"))
+        std::fprintf(stderr, "[labs] dev %d: kernel %d, L=%d, lanes/walk %d, R %d, %d blocks/SM of %d walks, "
+                     "%d B shared per block, resident %lld walks\n", dev, wp.kernel, wp.L, wp.lpw, wp.R, bps,
+                     wp.walks_per_block, static_cast<int>(walk_smem_bytes(wp)),
+                     static_cast<long long>(resident));
     ring_slots = ring_slots_from_env();
     for (Slot& S : slot_) {
         S.ctr.reserve(4);

@@ -83,7 +83,7 @@ __global__ void saw_seed_kernel(SeedParams P) {
 // ---------------------------------------------------------------------------
 // host-side launchers (called from the C++ orchestration)
 size_t walk_smem_bytes(const WalkParams& P) {
-    return (size_t)(P.fm_words + P.walks_per_block * P.warp_words) * 4;
+    return (size_t)(P.fm_words + P.walks_per_block * P.warp_words) * 4;  // (warp_words: per walk)
 }
 
 cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int* score_out,
@@ -129,7 +129,7 @@ int walk_blocks_per_sm(WalkParams& P) {
     const int n_l1 = walk_blocks_for(P);
     WalkParams Q = P;
     Q.fm_words = (6 * P.kp1 + 3) / 4 * 4;
-    if (walk_blocks_for(Q) >= n_l1 && (Q.fm_words + Q.walks_per_block * Q.warp_words) * 4 <= 227 * 1024) {
+    if (walk_blocks_for(Q) >= n_l1 && walk_smem_bytes(Q) <= 227 * 1024) {
         P.fm_words = Q.fm_words;
         return walk_blocks_for(Q);
     }

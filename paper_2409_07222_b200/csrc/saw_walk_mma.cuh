@@ -27,6 +27,12 @@
 #pragma once
 #include "saw_walk.cuh"
 
+#ifndef LABS_MMA_MINB
+#define LABS_MMA_MINB 5  // resident 128-thread blocks per SM the register budget targets (NQ = 1):
+                         // 96 registers (a few spilled) -- 20 walks per SM beat 16 at 128
+                         // registers by 5 % (L=451) and 4 % (L=527)
+#endif
+
 namespace labs_b200 {
 
 __device__ __forceinline__ void mma_s8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -42,7 +48,7 @@ __device__ __forceinline__ void mma_s8(int (&d)[4], const uint32_t (&a)[4], uint
 // memory.
 struct MmaSmem {
     uint32_t* base;
-    int off_x1, off_xc, xwords;
+    int off_x1, off_xc, xcw;
     uint32_t* KL;        // correlation kernel, low / high bytes (byte koff + d = C_{2|d|})
     uint32_t* KH;
     uint32_t* C16;       // (initialisation only, inside the Bloom words)
@@ -51,9 +57,9 @@ struct MmaSmem {
     uint32_t* bloom;
     __device__ __forceinline__ uint32_t* Xw(int par) const { return base + par * off_x1; }
     __device__ __forceinline__ int8_t* X(int par) const { return reinterpret_cast<int8_t*>(Xw(par)); }
-    // copy c of parity par: byte j = X(par) byte j + c (copy 0 is X(par) itself)
+    // copy c (1..3) of parity par: word i = X(par) bytes xcl + 4i + c .. +3
     __device__ __forceinline__ uint32_t* Xc(int par, int c) const {
-        return c == 0 ? Xw(par) : base + off_xc + (par * 3 + c - 1) * xwords;
+        return base + off_xc + (par * 3 + c - 1) * xcw;
     }
 };
 
@@ -151,14 +157,12 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     }
     for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
     __syncwarp();
-    for (int wi = sl; wi < 6 * P.xwords; wi += LPW) {  // copies c = 1..3 of both parities
-        const int par = wi / (3 * P.xwords);
-        const int rem = wi - par * 3 * P.xwords;
-        const int c = 1 + rem / P.xwords;
-        const int word = rem - (c - 1) * P.xwords;
-        const uint32_t lo = w.Xw(par)[word];
-        const uint32_t hi = word + 1 < P.xwords ? w.Xw(par)[word + 1] : 0u;
-        w.Xc(par, c)[word] = prmt(lo, hi, sel4(c));
+    for (int wi = sl; wi < 6 * P.xcw; wi += LPW) {  // copies c = 1..3 of both parities
+        const int par = wi / (3 * P.xcw);
+        const int rem = wi - par * 3 * P.xcw;
+        const int c = 1 + rem / P.xcw;
+        const int word = rem - (c - 1) * P.xcw + (P.xcl >> 2);
+        w.Xc(par, c)[word - (P.xcl >> 2)] = prmt(w.Xw(par)[word], w.Xw(par)[word + 1], sel4(c));
     }
 
     // ---- exact C_{2t} of the owned lag words (registers), E, max|C| ----
@@ -226,9 +230,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     // B (parity) words: byte xoff + gq + 4tq - 7 - delta of X_par, from copy c
     const int jb = P.xoff + gq + 4 * tq - 7 - P.kdelta;
     const int cb = jb & 3;
-    const int xb = (jb - cb) >> 2;
-    const uint32_t* xc0 = w.Xc(0, cb);
-    const uint32_t* xc1 = w.Xc(1, cb);
+    const int xb = cb == 0 ? jb >> 2 : (jb - cb - P.xcl) >> 2;
+    const uint32_t* xc0 = cb == 0 ? w.Xw(0) : w.Xc(0, cb);
+    const uint32_t* xc1 = cb == 0 ? w.Xw(1) : w.Xc(1, cb);
     const bool one_key = L <= 1001;
     const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
@@ -544,8 +548,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         //     (lanes 0-3: x_a* in copy 0-3, lanes 4-7: x_b*), toggle the half bit (lane 8)
         if (sl < 8 && !(cen && sl >= 4)) {
             const int c = sl & 3;
-            const int pos = P.xoff + ((sl < 4) ? ah : (bstar >> 1)) - c;
-            reinterpret_cast<int8_t*>(w.Xc(apar, c))[pos] = (int8_t)((sl < 4) ? -xa : -xb);
+            const int pos = P.xoff + ((sl < 4) ? ah : (bstar >> 1));
+            int8_t* dst = c == 0 ? w.X(apar) + pos : reinterpret_cast<int8_t*>(w.Xc(apar, c)) + pos - c - P.xcl;
+            *dst = (int8_t)((sl < 4) ? -xa : -xb);
         }
         if (sl == 8) w.half[as >> 5] ^= 1u << (as & 31);
         if (dbg) {
@@ -614,7 +619,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 }
 
 template <int NQ, bool COUNT>
-__global__ void __launch_bounds__(128, NQ == 1 ? 4 : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
+__global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     const uint64_t* fm = P.fm;
     if (P.fm_words) {
@@ -629,7 +634,7 @@ __global__ void __launch_bounds__(128, NQ == 1 ? 4 : 3) saw_walk_mma_kernel(Walk
     w.base = base;
     w.off_x1 = P.off_x1;
     w.off_xc = P.off_xc;
-    w.xwords = P.xwords;
+    w.xcw = P.xcw;
     w.KL = base + P.off_kl;
     w.KH = base + P.off_kh;
     w.C16 = base + P.off_c16;
