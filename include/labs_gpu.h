@@ -137,6 +137,8 @@ typedef struct labs_saw_derived {
     uint64_t bloom_bits;
     int32_t free_bits;         /* k + 1 - p */
     int32_t neighbours_per_lane;
+    int32_t kernel;            /* walk kernel: 0 = K1 (IDP4A G), 1 = K1t (mma.sync int8 G) */
+    int32_t lanes_per_walk;
 } labs_saw_derived;
 int labs_saw_derive(const labs_saw_config* cfg, labs_saw_derived* out);
 
@@ -203,6 +205,10 @@ void labs_bench_destroy(labs_bench_plan* plan);
  * IADD3/LOP3/SHF-only and a 1:1 mix, and IDP4A lane-instructions/s (each = 4 int8 MACs). */
 int labs_int32_peak(double* imad_ops, double* ialu_ops, double* mixed_ops, double* dp4a_ops,
                     int32_t* sm_count, int32_t* clock_khz);
+
+/* int8 tensor-core MAC rate: mma.sync.m16n8k32.s8 chains on every SM (the path K1t's
+ * sliding dot products use); MACs per second. */
+int labs_imma_peak(double* int8_macs_per_s);
 
 /* Host-side helpers (no GPU needed): the formats and hashes the sink chain uses. */
 uint64_t labs_canonical_hash(const int8_t* signs, int32_t n, int32_t table); /* rng.hpp:89-95 */

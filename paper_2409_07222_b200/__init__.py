@@ -29,6 +29,7 @@ from .api import (  # noqa: F401
     expand_skew,
     format_record,
     hex_encode,
+    imma_peak,
     int32_peak,
     library_path,
     load_library,
@@ -44,6 +45,6 @@ __all__ = [
     "Candidate", "CandidateSink", "CollectingSink", "DedupSink", "LabsError", "PoolStats",
     "SawConfig", "WalkResult", "bench_plan", "canonical_hash", "rank_prefixes", "derive", "device_count",
     "energy_threshold_for_merit", "enumerate_class", "expand_skew", "format_record",
-    "hex_encode", "int32_peak", "library_path", "load_library", "merit_factor", "pq_score",
+    "hex_encode", "imma_peak", "int32_peak", "library_path", "load_library", "merit_factor", "pq_score",
     "run_saw_pool", "saw_walks", "skew_flip_deltas",
 ]

@@ -81,6 +81,8 @@ class _Derived(C.Structure):
         ("prefix_len", C.c_int32), ("bloom_hashes", C.c_int32), ("iterations", C.c_int64),
         ("energy_threshold", C.c_int64), ("bloom_bits", C.c_uint64), ("free_bits", C.c_int32),
         ("neighbours_per_lane", C.c_int32),
+        ("kernel", C.c_int32),
+        ("lanes_per_walk", C.c_int32),
     ]
 
 
@@ -156,6 +158,7 @@ def load_library():
                                       C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
         lib.labs_int32_peak.argtypes = [C.POINTER(C.c_double)] * 4 + [C.POINTER(C.c_int32)] * 2
         lib.labs_device_count.argtypes = [C.POINTER(C.c_int32)]
+        lib.labs_imma_peak.argtypes = [C.POINTER(C.c_double)]
         lib.labs_canonical_hash.restype = C.c_uint64
         lib.labs_canonical_hash.argtypes = [C.POINTER(C.c_int8), C.c_int32, C.c_int32]
         lib.labs_format_record.argtypes = [C.POINTER(C.c_int8), C.c_int32, C.c_int64, C.c_char_p,
@@ -534,6 +537,14 @@ def int32_peak() -> dict:
     _check(lib.labs_int32_peak(*[C.byref(x) for x in v], C.byref(sm), C.byref(clk)))
     return dict(imad=v[0].value, ialu=v[1].value, mixed=v[2].value, dp4a=v[3].value,
                 sm_count=sm.value, clock_khz=clk.value)
+
+
+def imma_peak() -> float:
+    """int8 tensor-core MACs/s (mma.sync m16n8k32.s8 over every SM)."""
+    lib = load_library()
+    v = C.c_double()
+    _check(lib.labs_imma_peak(C.byref(v)))
+    return v.value
 
 
 def device_count() -> int:

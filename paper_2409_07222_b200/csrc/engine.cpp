@@ -845,6 +845,8 @@ int labs_saw_derive(const labs_saw_config* cfg, labs_saw_derived* out) {
     out->bloom_bits = d.bloom_bits;
     out->free_bits = d.kp1 - d.p;
     out->neighbours_per_lane = err.empty() ? wp.R : 0;
+    out->kernel = err.empty() ? wp.kernel : 0;
+    out->lanes_per_walk = err.empty() ? wp.lpw : 0;
     if (!err.empty()) {
         set_error(err);
         return LABS_EINVAL;

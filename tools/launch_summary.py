@@ -19,12 +19,12 @@ tot = sum(t for _, t in agg.values())
 tag = sys.argv[2] if len(sys.argv) > 2 else ""
 print(f"# {tag} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400`\n")
 print("Command: `python bench.py --steps 2 --warmup 1 --restarts 8 --no-cpu-baseline` (L=451, 8192 walks per")
-print("launch; the `k_*` launches are the in-run INT32/IDP4A peak microbenchmark).  Cold-cache")
+print("launch; the `k_*` launches are the in-run INT32/IDP4A/IMMA peak microbenchmarks).  Cold-cache")
 print("serialised times: compare shares, not absolutes.\n")
 print("| kernel | launches | total ms | share |\n|---|---|---|---|")
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"| {k.split('(')[0]} | {n} | {t:.3f} | {100 * t / tot:.1f}% |")
-walk = sum(t for k, (n, t) in agg.items() if "saw_walk_kernel" in k and ", 0>" in k)
+walk = sum(t for k, (n, t) in agg.items() if "saw_walk" in k and (", 0>" in k or ", false>" in k))
 seed = sum(t for k, (n, t) in agg.items() if "seed" in k)
 print(f"\nPer timed step the walk kernel is {100 * walk / (walk + seed):.2f}% of the device time "
       "(seed kernel the rest; the `<..., 1>` launch is the untimed delta-counting pass).")

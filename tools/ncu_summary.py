@@ -14,6 +14,8 @@ ap.add_argument("--json", default=None)
 ap.add_argument("--walks", type=int, default=0)
 ap.add_argument("--label", default="")
 ap.add_argument("--source", default="")
+ap.add_argument("--round", default="r02")
+ap.add_argument("--iterations", type=float, default=0, help="walk iterations in the launch")
 a = ap.parse_args()
 
 out = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True,
@@ -30,6 +32,10 @@ def nbytes(n):
 
 
 KEYS = ["gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -51,7 +57,7 @@ if a.json:
     dram = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
     f = lambda n: float(get(n))  # noqa: E731
     summary = {
-        "round": "r01", "kernel": a.label, "source": a.source,
+        "round": a.round, "kernel": a.label, "source": a.source,
         "walk_kernel_dram_bytes_per_walk": round(dram / a.walks, 2) if a.walks else None,
         "walk_kernel_dram_bytes_per_launch_profiled": dram,
         "walks_per_launch_profiled": a.walks,
@@ -59,6 +65,13 @@ if a.json:
         "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "pipe_alu_pct": f("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
         "pipe_fma_pct": f("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+        "pipe_fma_cycles_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+        "pipe_fmaheavy_cycles_pct": f("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+        "pipe_alu_cycles_pct": f("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+        "pipe_tensor_imma_cycles_pct": f("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active"),
+        "warp_instructions": f("smsp__inst_executed.sum"),
+        "warp_instructions_per_walk_iteration":
+            round(f("smsp__inst_executed.sum") / a.iterations, 1) if a.iterations else None,
         "pipe_lsu_pct": f("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
         "achieved_occupancy_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers_per_thread": f("launch__registers_per_thread"),
