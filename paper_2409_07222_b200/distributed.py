@@ -21,7 +21,7 @@ from typing import Callable, Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .api import Candidate, CandidateSink, PoolStats, SawConfig, run_saw_pool
+from .api import Candidate, CandidateSink, PoolStats, SawConfig, canonical_hash, run_saw_pool
 
 # stats merged by sum / by min (PoolStats fields, saw.hpp:161-167 + GPU counters)
 _SUM_KEYS = ("walks", "iterations", "emitted_raw", "delta_evals_computed", "exhausted_walks",
@@ -51,9 +51,11 @@ def merge_shards(parts: Iterable[Sequence[Candidate]],
                  hash_fn: Optional[Callable[[np.ndarray], object]] = None) -> List[Candidate]:
     """Merge per-shard candidate lists into the single-pool --threads 1 order with dedup.
 
-    `hash_fn` defaults to the exact sequence bytes; pass canonical_hash for the reference's
-    64-bit DedupSink key (identical unless the tabulation hash collides)."""
-    h = hash_fn or _key
+    The dedup key is the reference DedupSink's: the 64-bit canonical_hash(0) of the full
+    sequence (candidate.hpp:84-99, rng.hpp:89-95), so even a tabulation-hash collision is
+    resolved as the reference resolves it (the later sequence is dropped).  `hash_fn`
+    replaces it (e.g. exact sequence bytes)."""
+    h = hash_fn or (lambda seq: canonical_hash(seq, 0))
     allc = [c for part in parts for c in part]
     allc.sort(key=lambda c: (c.walker, c.restart, c.iteration))
     seen, out = set(), []

@@ -103,3 +103,20 @@ def test_shard_config_rejects_coupled_modes():
         shard_config(SawConfig(length=51, target_merit=3.0, candidate_quota=5), 0, 2)
     c = shard_config(SawConfig(length=51, target_merit=3.0), 1, 2)
     assert (c.shard_index, c.shard_count) == (1, 2)
+
+
+def test_merge_shards_dedups_by_canonical_hash(monkeypatch):
+    # DedupSink semantics (candidate.hpp:84-99): the key is canonical_hash(0), so two
+    # different sequences whose hashes collide keep only the first -- forced here by a
+    # colliding hash function standing in for the tabulation hash
+    from paper_2409_07222_b200 import distributed as D
+    from paper_2409_07222_b200.api import Candidate
+
+    a = Candidate(np.array([1, 1, -1], np.int8), 5, "saw", np.zeros(0, np.int8), 0, 0, 1)
+    b = Candidate(np.array([1, -1, -1], np.int8), 5, "saw", np.zeros(0, np.int8), 1, 0, 1)
+    c = Candidate(np.array([1, 1, -1], np.int8), 5, "saw", np.zeros(0, np.int8), 2, 0, 3)
+    merged = D.merge_shards([[b], [c, a]])
+    assert [m.walker for m in merged] == [0, 1]  # (walker, restart, iteration) order; c dropped
+    monkeypatch.setattr(D, "canonical_hash", lambda seq, t=0: 42)
+    merged = D.merge_shards([[b], [c, a]])
+    assert [m.walker for m in merged] == [0]  # colliding hashes: only the first survives
