@@ -25,7 +25,7 @@ namespace labs_b200 {
 
 namespace {
 constexpr int kPqWarps = 8;            // warps (neighbours) per block
-constexpr int kPqMaxL = kMaxHalf;      // L <= 1023 (tabulation range)
+constexpr int kPqMaxL = kMaxHalf;      // L <= 1024 (TabulationHash::kMaxLen, rng.hpp:77)
 constexpr int kPqLagsPerLane = (kPqMaxL + 31) / 32;
 
 __device__ __forceinline__ int warp_sum_i(int v) {
@@ -161,8 +161,11 @@ __global__ void __launch_bounds__(32 * kPqWarps) pq_score_kernel(const __grid_co
     }
 }
 
-// Per-thread device context: refine_batch (pipeline.cpp:132-186) runs refines on several
-// host threads at once, each gets its own stream and buffers.
+// Per-thread device contexts: refine_batch (pipeline.cpp:132-186) runs refines on several
+// host threads at once, each gets its own streams and buffers.  refine_with_operators
+// (pq.cpp:203-228) alternates lengths L-1, L, L+1, so a thread keeps a small cache of
+// contexts keyed by (device, L, T_r) instead of freeing and reallocating -- cudaFree and
+// cudaFreeHost synchronise the whole device, across every refine thread.
 struct PqCtx {
     int dev = -1;
     cudaStream_t st = nullptr;
@@ -192,7 +195,13 @@ struct PqCtx {
         t_r = -1;
     }
 };
-thread_local PqCtx g_pq;
+constexpr int kPqCtxCache = 6;
+struct PqCache {
+    PqCtx ctx[kPqCtxCache];
+    uint64_t used[kPqCtxCache] = {};
+    uint64_t clock = 0;
+};
+thread_local PqCache g_pq;
 
 #define PQ_CUDA(call)                                                          \
     do {                                                                       \
@@ -203,11 +212,32 @@ thread_local PqCtx g_pq;
         }                                                                      \
     } while (0)
 
-int pq_prepare(int L, int t_r) {
-    PqCtx& c = g_pq;
+int pq_init(PqCtx& c, int dev, int L, int t_r);
+
+PqCtx* pq_prepare(int L, int t_r, int* rc) {
     int dev = 0;
-    PQ_CUDA(cudaGetDevice(&dev));
-    if (c.st && c.L == L && c.t_r == t_r && c.dev == dev) return LABS_OK;
+    *rc = LABS_OK;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        set_error("pq_score: cudaGetDevice failed");
+        *rc = LABS_ECUDA;
+        return nullptr;
+    }
+    PqCache& cache = g_pq;
+    int slot = 0;
+    for (int i = 0; i < kPqCtxCache; ++i) {
+        const PqCtx& c = cache.ctx[i];
+        if (c.st && c.L == L && c.t_r == t_r && c.dev == dev) {
+            cache.used[i] = ++cache.clock;
+            return &cache.ctx[i];
+        }
+        if (cache.used[i] < cache.used[slot]) slot = i;  // least recently used (or empty)
+    }
+    *rc = pq_init(cache.ctx[slot], dev, L, t_r);
+    cache.used[slot] = ++cache.clock;
+    return *rc == LABS_OK ? &cache.ctx[slot] : nullptr;
+}
+
+int pq_init(PqCtx& c, int dev, int L, int t_r) {
     c.release();
     c.dev = dev;
     PQ_CUDA(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
@@ -236,8 +266,8 @@ int pq_prepare(int L, int t_r) {
 
 int pq_score(int L, int t_r, const int8_t* pivot, int32_t* delta, int32_t* rot_e,
              uint64_t* rot_h, int64_t* pivot_energy) {
-    if (L < 3 || L > kPqMaxL - 1) {
-        set_error("pq_score: length must be in [3, 1023]");
+    if (L < 3 || L > kPqMaxL) {
+        set_error("pq_score: length must be in [3, 1024]");
         return LABS_EINVAL;
     }
     if (t_r < 0 || t_r >= L) {
@@ -249,9 +279,10 @@ int pq_score(int L, int t_r, const int8_t* pivot, int32_t* delta, int32_t* rot_e
         set_error("no CUDA device available (the Step-2 scorer has no CPU fallback)");
         return LABS_ENODEV;
     }
-    const int rc = pq_prepare(L, t_r);
-    if (rc != LABS_OK) return rc;
-    PqCtx& c = g_pq;
+    int rc = LABS_OK;
+    PqCtx* cp = pq_prepare(L, t_r, &rc);
+    if (!cp) return rc;
+    PqCtx& c = *cp;
     std::memcpy(c.h_pivot, pivot, static_cast<size_t>(L));
     PQ_CUDA(cudaMemcpyAsync(c.d_pivot, c.h_pivot, L, cudaMemcpyHostToDevice, c.st));
     PqLaunch P{};

@@ -109,3 +109,23 @@ def test_verify_flags_corrupted_record(tmp_path):
     assert r.returncode == 1
     assert "2 records, 1 mismatches, 1 malformed" in r.stdout
     assert "energy mismatch" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exe", [SOLVE_S1, SOLVE_B200], ids=["gpu_step1", "gpu_step1_step2"])
+def test_solve_multithreaded_matches_reference(tmp_path, exe):
+    # --threads 4: the reference's Step-1 pool and refine_batch (pipeline.cpp:132-186) then
+    # run concurrently, so emission order and equal-energy ties are timing-dependent even
+    # for the reference; the candidate SET, the best energy per target length and the Step-1
+    # statistics must match.  Exercises K5's per-thread context cache (refine threads
+    # alternate lengths L-1, L, L+1 through refine_with_operators).
+    if not os.access(SOLVE_REF, os.X_OK):
+        pytest.skip("reference solve not built")
+    a = ("-L 62 --rounds 2 --walkers 16 --restarts 3 --target-f 4.0 --refine-top 6 --tu 120 "
+         "--tr 4 --seed 11 --threads 4 --deterministic --no-construct").split()
+    got = _run(exe, a, tmp_path, "b200")
+    want = _run(SOLVE_REF, a, tmp_path, "ref")
+    assert sorted(got[3].splitlines()) == sorted(want[3].splitlines())   # candidate set
+    best = lambda txt: sorted(tuple(l.split("\t")[:2]) for l in txt.splitlines() if l)  # noqa: E731
+    assert best(got[2]) == best(want[2])                                 # (L, E) per target
+    assert got[1].split(" wall=")[0].split("calls=")[0] == want[1].split(" wall=")[0].split("calls=")[0]
