@@ -224,6 +224,32 @@ def gpu_parity(labs, ref, walkers):
                         "its run_walk + DedupSink in --threads 1 order (oracle/_ref)"}
 
 
+def enum_c2(labs, peak, m=32):
+    """BASELINE config 2: K4 Gray enumeration of restriction class 0
+    at L=201, p=12, over the lowest m free half positions (the rest +1), sieve F >= 5.0.
+    Roofline: the FMA pipe (IDP4A + IMAD share it, 64 lanes/clk/SM): per Gray step every
+    even lag takes two IDP4A (its dc) and one IMAD (dc (2C + dc)), i.e. 3 FMA-pipe
+    lane-ops per lag, (L-1)/2 lags."""
+    L2, p2, cls, e_l = 201, 12, 0, 4040
+    labs.enumerate_class(L2, p2, cls, 20, e_l, collect=False)  # warm-up
+    hits, st = labs.enumerate_class(L2, p2, cls, m, e_l, collect=False)
+    steps_s = st["configurations"] / (st["kernel_ms"] / 1e3)
+    fma_per_step = 3 * (L2 - 1) // 2
+    achieved = steps_s * fma_per_step
+    peak_fma = peak["dp4a"] if peak else None
+    return {"workload": f"C2: L={L2} p={p2} class {cls}, Gray range over {m} free half positions "
+                        f"(2^{m} configurations), E < {e_l} (F >= 5.0)",
+            "gray_steps_per_s": steps_s, "lag_updates_per_s": steps_s * (L2 - 1) // 2,
+            "kernel_ms": st["kernel_ms"], "best_energy": st["best_energy"],
+            "emitted": st["emitted"],
+            "roofline": {"bound": "fma_pipe", "achieved": achieved, "peak": peak_fma,
+                         "unit": "lane-ops/s", "frac": achieved / peak_fma if peak_fma else None,
+                         "per_step": f"{fma_per_step} FMA-pipe lane-ops (2 IDP4A + 1 IMAD per "
+                                     f"even lag)",
+                         "peak_source": "measured in this run: IDP4A lane-instr/s (the FMA "
+                                        "pipe's issue rate, labs_int32_peak)"}}
+
+
 def run_reference_arm(args, ws, rank):
     if rank != 0:
         return
@@ -260,6 +286,7 @@ def main():
     ap.add_argument("--restarts", type=int, default=RESTARTS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 enumeration keys")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
@@ -428,6 +455,7 @@ def main():
                     "path": "paper_2409_07222_b200.run_saw_pool -> C ABI labs_saw_pool_run "
                             "(host seed tables in, deduplicated candidates out)"},
             "clocks": clk,
+            "c2_enumeration": enum_c2(labs, peak) if not args.no_c2 else None,
         }
         print(json.dumps(line), flush=True)
     plan.close()
