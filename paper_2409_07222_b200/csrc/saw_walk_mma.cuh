@@ -125,6 +125,61 @@ __device__ __forceinline__ void g_mma(const uint32_t* __restrict__ Kw, int nks, 
             for (int i = 0; i < 4; ++i) acc[j][p][i] += ac2[j][p][i];
 }
 
+// Fully unrolled k-step loop for a compile-time nks (the common lengths): no loop control
+// and no register moves for the a0/a2 rotation.
+template <int NQ, int NKS>
+__device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int kidx0, int xb,
+                                            const uint32_t* __restrict__ xc0,
+                                            const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
+    int ac2[NQ][2][4];
+    uint32_t w0[NQ][NKS + 2], w2[NQ][NKS + 2];  // a0 / a2 words of steps -2 .. NKS-1
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+#pragma unroll
+        for (int s = -2; s < NKS; ++s) {
+            w0[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s];
+            w2[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s + 4];
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ac2[j][p][i] = 0;
+    }
+#pragma unroll
+    for (int s = 0; s < NKS; ++s) {
+        const uint32_t b00 = xc0[xb + 8 * s], b01 = xc0[xb + 8 * s + 4];
+        const uint32_t b10 = xc1[xb + 8 * s], b11 = xc1[xb + 8 * s + 4];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+            const uint32_t a[4] = {w0[j][s + 2], w0[j][s], w2[j][s + 2], w2[j][s]};
+            if ((s & 1) == 0) {
+                mma_s8(acc[j][0], a, b00, b01);
+                mma_s8(acc[j][1], a, b10, b11);
+            } else {
+                mma_s8(ac2[j][0], a, b00, b01);
+                mma_s8(ac2[j][1], a, b10, b11);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][p][i] += ac2[j][p][i];
+}
+
+template <int NQ>
+__device__ __forceinline__ void g_mma_any(const uint32_t* __restrict__ Kw, int nks, int kidx0, int xb,
+                                          const uint32_t* __restrict__ xc0,
+                                          const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
+    switch (nks) {  // (warp-uniform)
+        case 8: g_mma_fixed<NQ, 8>(Kw, kidx0, xb, xc0, xc1, acc); break;
+        case 10: g_mma_fixed<NQ, 10>(Kw, kidx0, xb, xc0, xc1, acc); break;
+        default: g_mma<NQ>(Kw, nks, kidx0, xb, xc0, xc1, acc); break;
+    }
+}
+
 template <int NQ, bool COUNT>
 __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64_t* fm0,
                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
@@ -309,7 +364,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 #pragma unroll
                 for (int i = 0; i < 4; ++i) acc[j][p2][i] = 0;
         if (wide) {  // G = 256 G_high + G_low
-            g_mma<NQ>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
+            g_mma_any<NQ>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
 #pragma unroll
             for (int j = 0; j < NQ; ++j)
 #pragma unroll
@@ -318,7 +373,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                     for (int i = 0; i < 4; ++i) acc[j][p2][i] *= 256;
             ++wide_iters;
         }
-        g_mma<NQ>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
+        g_mma_any<NQ>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
         // ---- exact deltas / keys: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
