@@ -521,13 +521,11 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             const int down = as - A0;
             const int ex3 = as + L - 1;
             const int aex = ex3 / 3;
-            const int dex = (ex3 - 3 * aex == 0 && (aex & 1) == apar && aex >= P.p) ? aex - A0 : -1;
+            // (warp-uniform: a* is; about one step in six has the excluded Q pair)
+            const bool has_ex = ex3 - 3 * aex == 0 && (aex & 1) == apar && aex >= P.p;
             const int mo = (down >= 0 && (down & kSlotMask) == 0)
                                ? (down >> 8) * 8 + (down & 1) * 4 + ((down >> 6) & 2) + ((down >> 1) & 1) : -1;
-            const int mx = (dex >= 0 && (dex & kSlotMask) == 0)
-                               ? (dex >> 8) * 8 + (dex & 1) * 4 + ((dex >> 6) & 2) + ((dex >> 1) & 1) : -1;
-            const int vo = 8 * xb * (int)Xa[ah - (k - as)];      // (unscaled corrections)
-            const int vx = mx >= 0 ? 8 * xa * (int)Xa[(2 * aex - as) >> 1] : 0;
+            const int vo = 8 * xb * (int)Xa[ah - (k - as)];      // (unscaled correction)
             skip = inval | (mo >= 0 ? 1u << mo : 0u);
             const int c0 = (k & 1) ? -mul : mul;  // c_a for e = 0 (A is even); alternates with e
             uint32_t sf[4], sg[4], sx[4];
@@ -558,9 +556,17 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                         v += vo;
                         xs[m] = -xs[m];
                     }
-                    if (m == mx) v += vx;
                     T[m] += (uint32_t)(v * sc8);
                 }
+            }
+            if (has_ex) {  // the pair excluded from Q(aex) passes through a*: take its term back
+                const int dex = aex - A0;
+                const int mx = (dex >= 0 && (dex & kSlotMask) == 0)
+                                   ? (dex >> 8) * 8 + (dex & 1) * 4 + ((dex >> 6) & 2) + ((dex >> 1) & 1) : -1;
+                const uint32_t vx = (uint32_t)(8 * sc8 * xa * (int)Xa[(2 * aex - as) >> 1]);
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    if (m == mx) T[m] += vx;
             }
         }
         // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
