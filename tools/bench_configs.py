@@ -35,7 +35,8 @@ def pool(name, L, p, F, walkers, restarts):
             "flip_delta_evals_per_s": cst.delta_evals / (ms / 1e3),
             "iterations_per_s": cst.iterations / (ms / 1e3),
             "candidates": st.emitted, "candidates_per_s": st.emitted / (ms / 1e3),
-            "neighbours_per_lane": labs.derive(labs.SawConfig(**base)).get("neighbours_per_lane")}
+            "neighbours_per_lane": labs.derive(labs.SawConfig(**base)).get("neighbours_per_lane"),
+            "walk_kernel": {0: "K1", 1: "K1t"}.get(labs.derive(labs.SawConfig(**base)).get("kernel"))}
 
 
 def enum_c2(m=36):
@@ -59,6 +60,14 @@ def main():
     ap.add_argument("--pools-only", action="store_true", help="skip C2 (kernel-variant A/B)")
     a = ap.parse_args()
     res = [pool(*c) for c in POOLS]
+    for c in POOLS:  # the other walk kernel on the same pools (policy A/B)
+        d = labs.derive(labs.SawConfig(length=c[1], walkers=c[4], prefix_len=c[2],
+                                       target_merit=c[3], max_restarts=c[5]))
+        os.environ["LABS_KERNEL"] = "dp4a" if d["kernel"] == 1 else "mma"
+        r = pool(c[0] + "-alt", *c[1:])
+        r["walk_kernel"] = os.environ["LABS_KERNEL"]
+        del os.environ["LABS_KERNEL"]
+        res.append(r)
     if not a.pools_only:
         res.insert(1, enum_c2(a.m))
     for r in res:
