@@ -357,6 +357,7 @@ JobOut DeviceRunner::finish(int s) {
     const unsigned long long head = S.h_ctr.p[0];
     const int* ctl = reinterpret_cast<const int*>(S.h_ctr.p + 3);
     S.busy = false;
+    if (ctl[0] & 2) throw CudaFailure("shared-memory bounds check failed (LABS_BOUNDS_CHECK build)");
     if (ctl[0]) throw CudaFailure("record ring drain stalled (no host drain for 20 s)");
     drain(S, head, true);
     S.seq0 += head;

@@ -771,7 +771,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
                     if (slot < tail + (unsigned long long)P.rec_cap) {
                         wait = false;
                     } else if (++spins >= kRingWaitSpins) {
-                        P.ctl[0] = 1;
+                        atomicOr(&P.ctl[0], 1);
                         wait = wrote = false;
                     }
                 }

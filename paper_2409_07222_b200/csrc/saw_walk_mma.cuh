@@ -35,6 +35,21 @@
 
 namespace labs_b200 {
 
+// Debug builds (-DLABS_BOUNDS_CHECK, `make OUT=../_lib_check EXTRA=-DLABS_BOUNDS_CHECK`) check
+// every shared-memory window index of K1t against its array and raise ctl[0] bit 1; the host
+// then fails the call ("shared-memory bounds check failed").  compute-sanitizer is not
+// available on this GPU pool, so the parity suite runs against that build as well.
+#ifdef LABS_BOUNDS_CHECK
+#define LABS_BC(P, i, lo, hi)                                                   \
+    do {                                                                        \
+        if ((i) < (lo) || (i) >= (hi)) atomicOr(const_cast<int*>(&(P).ctl[0]), 2); \
+    } while (0)
+#else
+#define LABS_BC(P, i, lo, hi) \
+    do {                      \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void mma_s8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -140,6 +155,7 @@ __device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int
             w0[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s];
             w2[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s + 4];
         }
+
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -288,6 +304,12 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     const int xb = cb == 0 ? jb >> 2 : (jb - cb - P.xcl) >> 2;
     const uint32_t* xc0 = cb == 0 ? w.Xw(0) : w.Xc(0, cb);
     const uint32_t* xc1 = cb == 0 ? w.Xw(1) : w.Xc(1, cb);
+    // (G's reads: kernel words kidx0 - 32 (NQ-1) - 16 .. kidx0 + 8 nks - 4, parity words
+    // xb .. xb + 8 nks - 4 of the primary array or a copy)
+    LABS_BC(P, kidx0 - 32 * (NQ - 1) - 16, 0, P.kwords);
+    LABS_BC(P, kidx0 + 8 * P.nks - 4, 0, P.kwords);
+    LABS_BC(P, xb, 0, cb == 0 ? P.xwords : P.xcw);
+    LABS_BC(P, xb + 8 * P.nks - 4, 0, cb == 0 ? P.xwords : P.xcw);
     const bool one_key = L <= 1001;
     const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
@@ -526,6 +548,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             const int mo = (down >= 0 && (down & kSlotMask) == 0)
                                ? (down >> 8) * 8 + (down & 1) * 4 + ((down >> 6) & 2) + ((down >> 1) & 1) : -1;
             const int vo = 8 * xb * (int)Xa[ah - (k - as)];      // (unscaled correction)
+            LABS_BC(P, P.xoff + ah - (k - as), 0, 4 * P.xwords);
             skip = inval | (mo >= 0 ? 1u << mo : 0u);
             const int c0 = (k & 1) ? -mul : mul;  // c_a for e = 0 (A is even); alternates with e
             uint32_t sf[4], sg[4], sx[4];
@@ -547,6 +570,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 const uint32_t wf = prmt(Xaw[bf >> 2], Xaw[(bf >> 2) + 1], sel4r(bf & 3));
                 const uint32_t wg = prmt(Xaw[bg >> 2], Xaw[(bg >> 2) + 1], sel4(bg & 3));
                 const uint32_t wx = prmt(Xaw[bx >> 2], Xaw[(bx >> 2) + 1], sel4(bx & 3));
+                LABS_BC(P, bf >> 2, 0, P.xwords - 1);
+                LABS_BC(P, bg >> 2, 0, P.xwords - 1);
+                LABS_BC(P, bx >> 2, 0, P.xwords - 1);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
@@ -587,6 +613,8 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 if (jj < nj && s < S) {
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
+                    LABS_BC(P, awF + s, 0, P.xwords - 1);
+                    LABS_BC(P, awB - s, 0, P.xwords - 1);
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
                         C[jj][b] = __dp4a((int)fw, e1h[b], __dp4a((int)bw, e1h[b], C[jj][b]));
@@ -636,7 +664,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 if (slot < tail + (unsigned long long)P.rec_cap) {
                     wait = false;
                 } else if (++spins >= kRingWaitSpins) {
-                    if (sl == 0) P.ctl[0] = 1;
+                    if (sl == 0) atomicOr(&P.ctl[0], 1);
                     wait = wrote = false;
                 } else {
                     __nanosleep(4000);
