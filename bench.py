@@ -310,6 +310,9 @@ def main():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     if os.environ.get("BENCH_SAME_DEVICE"):
         local = 0
+    # (the max / sum reductions of the per-rank timings: on the device under NCCL, on the
+    # host under gloo)
+    red_dev = "cpu" if dist is not None and dist.get_backend() == "gloo" else "cuda"
     torch.cuda.set_device(local)
 
     walkers = args.walkers_per_gpu * ws
@@ -340,7 +343,7 @@ def main():
     clk = clocks.stop(t0, t1) if clocks else None
 
     vals = torch.tensor([ms_step, float(deltas_rank), float(st.emitted), float(iters_rank),
-                         st.kernel_ms, float(st.walks)], dtype=torch.float64, device="cuda")
+                         st.kernel_ms, float(st.walks)], dtype=torch.float64, device=red_dev)
     if dist is not None:
         mx, sm = vals.clone(), vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -365,7 +368,7 @@ def main():
         dt = time.perf_counter() - ta
         if i > 0:
             e2e_times.append(dt)
-    e2e_t = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=red_dev)
     if dist is not None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = e2e_t.item()

@@ -1,10 +1,13 @@
-"""bench.py's launch contract on CPU: the reference arm under torchrun (N=2, gloo) prints
-exactly one JSON line from rank 0 with the contract's keys, and every rank exits 0."""
+"""bench.py's launch contract: the reference arm under torchrun (N=2, gloo) on CPU, and the
+b200 arm under torchrun (N=2 on one B200, -m gpu) print exactly one JSON line from rank 0
+with the contract's keys, and every rank exits 0."""
 import json
 import os
 import socket
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -45,3 +48,20 @@ def test_reference_arm_torchrun_two_ranks():
               "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"], {})
     assert r.returncode == 0, r.stderr[-2000:]
     _check_line(r.stdout, 2)
+
+
+@pytest.mark.gpu
+def test_b200_arm_torchrun_two_ranks_one_device():
+    # the N>1 b200 arm: torchrun world 2 (both ranks on the one B200, gloo for the
+    # reductions), class shards per rank, max-over-ranks timing; one JSON line from rank 0
+    r = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py",
+              "--gpus", "2", "--steps", "1", "--warmup", "1", "--walkers-per-gpu", "128",
+              "--restarts", "2", "--no-cpu-baseline", "--no-c2", "--e2e-steps", "1"],
+             {"BENCH_SAME_DEVICE": "1", "BENCH_DIST_BACKEND": "gloo"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["walks_per_step"] == 2 * 128 * 2
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
