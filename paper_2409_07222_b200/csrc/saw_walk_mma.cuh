@@ -196,6 +196,41 @@ __device__ __forceinline__ void g_mma_any(const uint32_t* __restrict__ Kw, int n
     }
 }
 
+// The T updates of the lane's 8 NQ neighbours for one step (see run_walk_mma (2)): per
+// group of four consecutive half indices A..A+3 three byte windows -- f, g and (for a*'s
+// parity APAR) p -- and one-hot IDP4A selectors.
+template <int APAR, int NQ>
+__device__ __forceinline__ void t_update_groups(const WalkParams& P, const uint32_t* Xaw, int A0,
+                                                int ah, const uint32_t (&sf)[4],
+                                                const uint32_t (&sg)[4], const uint32_t (&sx)[4],
+                                                int mo, int vo, int sc8, uint32_t (&T)[8 * NQ],
+                                                int (&xs)[8 * NQ]) {
+    const int k = P.k;
+#pragma unroll
+    for (int grp = 0; grp < 2 * NQ; ++grp) {
+        const int Aa = min(A0 + 128 * grp, k);  // (addresses of invalid groups stay in range)
+        const int bf = P.xoff + ah + k - Aa - 3, bg = P.xoff + ah - k + Aa,
+                  bx = P.xoff + Aa - ah - APAR;
+        const uint32_t wf = prmt(Xaw[bf >> 2], Xaw[(bf >> 2) + 1], sel4r(bf & 3));
+        const uint32_t wg = prmt(Xaw[bg >> 2], Xaw[(bg >> 2) + 1], sel4(bg & 3));
+        const uint32_t wx = prmt(Xaw[bx >> 2], Xaw[(bx >> 2) + 1], sel4(bx & 3));
+        LABS_BC(P, bf >> 2, 0, P.xwords - 1);
+        LABS_BC(P, bg >> 2, 0, P.xwords - 1);
+        LABS_BC(P, bx >> 2, 0, P.xwords - 1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
+            const int vp = (e & 1) == APAR ? __dp4a((int)wx, (int)sx[e], 0) : 0;
+            int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e], vp));
+            if (m == mo) {
+                v += vo;
+                xs[m] = -xs[m];
+            }
+            T[m] += (uint32_t)(v * sc8);
+        }
+    }
+}
+
 template <int NQ, bool COUNT>
 __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64_t* fm0,
                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
@@ -562,29 +597,10 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             }
             const uint32_t* Xaw = w.Xw(apar);
             const int sc8 = 8 * sc;
-#pragma unroll
-            for (int grp = 0; grp < 2 * NQ; ++grp) {
-                const int Aa = min(A0 + 128 * grp, k);  // (addresses of invalid groups stay in range)
-                const int bf = P.xoff + ah + k - Aa - 3, bg = P.xoff + ah - k + Aa,
-                          bx = P.xoff + Aa - ah - apar;
-                const uint32_t wf = prmt(Xaw[bf >> 2], Xaw[(bf >> 2) + 1], sel4r(bf & 3));
-                const uint32_t wg = prmt(Xaw[bg >> 2], Xaw[(bg >> 2) + 1], sel4(bg & 3));
-                const uint32_t wx = prmt(Xaw[bx >> 2], Xaw[(bx >> 2) + 1], sel4(bx & 3));
-                LABS_BC(P, bf >> 2, 0, P.xwords - 1);
-                LABS_BC(P, bg >> 2, 0, P.xwords - 1);
-                LABS_BC(P, bx >> 2, 0, P.xwords - 1);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
-                    int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e],
-                                                                __dp4a((int)wx, (int)sx[e], 0)));
-                    if (m == mo) {
-                        v += vo;
-                        xs[m] = -xs[m];
-                    }
-                    T[m] += (uint32_t)(v * sc8);
-                }
-            }
+            if (apar)  // (warp-uniform: the x_{2a-a*} term exists for a* 's parity only)
+                t_update_groups<1, NQ>(P, Xaw, A0, ah, sf, sg, sx, mo, vo, sc8, T, xs);
+            else
+                t_update_groups<0, NQ>(P, Xaw, A0, ah, sf, sg, sx, mo, vo, sc8, T, xs);
             if (has_ex) {  // the pair excluded from Q(aex) passes through a*: take its term back
                 const int dex = aex - A0;
                 const int mx = (dex >= 0 && (dex & kSlotMask) == 0)
