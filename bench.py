@@ -106,6 +106,27 @@ class Clocks:
                 "samples": len(sm)}
 
 
+ISSUE_PEAK_NOTE = ("warp-instructions per unit from the committed ncu capture (profiles/*.json, "
+                   "smsp__inst_executed.sum / units) x units/s, over the issue peak: one "
+                   "warp-instruction per cycle per SMSP = 4 x SMs x SM clock")
+
+
+def issue_roofline(units_per_s, profile, key, peak_info):
+    """The binding resource of K1t / K4: instruction issue.  Instructions per unit come
+    from the committed ncu capture; the peak is 4 SMSPs x SMs x the SM clock."""
+    try:
+        with open(os.path.join(ROOT, "profiles", profile)) as f:
+            per_unit = json.load(f).get(key)
+    except (OSError, ValueError):
+        per_unit = None
+    if not per_unit or not peak_info:
+        return None
+    peak = 4 * peak_info["sm_count"] * peak_info["clock_khz"] * 1e3
+    achieved = units_per_s * per_unit
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-instr/s",
+            "frac": achieved / peak, "per_unit": per_unit, "source": ISSUE_PEAK_NOTE}
+
+
 def ncu_traffic(walks):
     """DRAM bytes per launch of the walk kernel: the committed ncu capture's bytes per walk
     (profiles/ncu_summary.json, dram__bytes_read.sum + dram__bytes_write.sum) x walks."""
@@ -247,7 +268,9 @@ def enum_c2(labs, peak, m=32):
                          "per_step": f"{fma_per_step} FMA-pipe lane-ops (2 IDP4A + 1 IMAD per "
                                      f"even lag)",
                          "peak_source": "measured in this run: IDP4A lane-instr/s (the FMA "
-                                        "pipe's issue rate, labs_int32_peak)"}}
+                                        "pipe's issue rate, labs_int32_peak)",
+                         "issue": issue_roofline(steps_s, "r02/enum_kernel_ncu.json",
+                                                 "warp_instructions_per_gray_step", peak)}}
 
 
 def run_reference_arm(args, ws, rank):
@@ -398,6 +421,8 @@ def main():
                            "peak_source": "measured in this run (labs_imma_peak): "
                                           "mma.sync.m16n8k32.s8 int8 MACs/s x 2 ops"},
                 "walk_kernel": {0: "K1 (IDP4A G)", 1: "K1t (mma.sync int8 G)"}.get(kern, kern),
+                "issue": issue_roofline(iters_rank / (st.kernel_ms / 1e3), "ncu_summary.json",
+                                        "warp_instructions_per_walk_iteration", peak),
                 "int32_peak_detail": peak,
                 "alg_ops_per_launch": alg_ops,
                 "alg_unit": f"(reference-equivalent delta evals + applies) x (L+1) ops: one "
