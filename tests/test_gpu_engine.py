@@ -190,3 +190,25 @@ dist.destroy_process_group()
     want = [f"{c.walker}\t{c.restart}\t{labs.format_record(c)}" for c in got]
     want.append(f"#{st.walks} {st.iterations} {st.emitted} {st.best_energy}")
     assert out.read_text().splitlines() == want
+
+
+def test_cli_saw_unlimited_restarts_searches_every_class(tmp_path, restated):
+    # `labs saw --restarts 0 --seconds 2` (the CLI's default --threads is the
+    # host's hardware concurrency, labs_main.cpp:21-28) searches every restriction class at
+    # once -- all 128 p=8 prefixes appear among the records -- and stops within the budget
+    exe = os.path.join(ROOT, "paper_2409_07222_b200", "_lib", "labs")
+    out = tmp_path / "c.tsv"
+    r = subprocess.run([exe, "saw", "-L", "101", "--walkers", "256", "--p", "8", "--restarts", "0",
+                        "--seconds", "2", "--target-f", "4.8", "--out", str(out)],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    recs = out.read_text().splitlines()
+    prefixes = set()
+    for line in recs:
+        hexs = line.split("\t")[3]
+        bits = bin(int(hexs, 16))[2:].zfill(101)
+        prefixes.add(bits[:8])  # s_0..s_7 = the class prefix (MSB-first, +1 -> 1)
+    assert len(prefixes) == 128, len(prefixes)
+    stats = dict(f.split("=") for f in r.stderr.split() if "=" in f)
+    assert float(stats["wall"].rstrip("s")) < 2.0 + 1.0
+    assert int(stats["walks"]) >= 256
