@@ -8,7 +8,8 @@
 // half positions [p, p+m); configuration g = Gray(g) (bit j set <=> position p+j is -1).
 // Every g in [g_begin, g_end) with E < E_l is emitted; best E and its first g reported.
 //
-// Layout: one warp = one chunk of 2^chunk_log2 consecutive g (grid-stride over chunks).
+// Layout: 4 lanes (up to 32 lag words) -- eight chunks per warp -- or 16 / 32 lanes = one
+// chunk of 2^chunk_log2 consecutive g each (chunks from an atomic queue).
 // Lanes own the even lags t = 4(lane + 32j) + 1 .. +4 (C_{2t} in registers); the
 // sequence lives in shared memory as two parity byte arrays.  A step's energy change
 //     dE = sum_t dc_t (2 C_{2t} + dc_t),   dc_t = mul * (x_{a+2t} + x_{a-2t} - [t = k-a] x_b)
@@ -30,6 +31,9 @@
 namespace labs_b200 {
 
 #define FULLMASK 0xffffffffu
+#ifndef LABS_ENUM_MINB
+#define LABS_ENUM_MINB 5  // resident 128-thread blocks per SM the 4-lane variants target (93 registers)
+#endif
 
 struct EnumLaunch {
     int32_t L, k, kp1, p, m;
@@ -253,7 +257,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
 }
 
 template <int NJ, int LPW>
-__global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P);
+__global__ void __launch_bounds__(128, LPW == 4 ? LABS_ENUM_MINB : 1) enum_kernel(const __grid_constant__ EnumLaunch P);
 
 // Launch with one wave of resident blocks (the occupancy limit per SM x SMs), capped by
 // the work; the chunk queue balances the rest.
@@ -269,7 +273,7 @@ void launch_enum(const EnumLaunch& P, size_t smem, cudaStream_t stream, int sms,
 }
 
 template <int NJ, int LPW>
-__global__ void __launch_bounds__(128) enum_kernel(const __grid_constant__ EnumLaunch P) {
+__global__ void __launch_bounds__(128, LPW == 4 ? LABS_ENUM_MINB : 1) enum_kernel(const __grid_constant__ EnumLaunch P) {
     extern __shared__ uint32_t esmem[];
     constexpr int SEGS = 32 / LPW;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -410,8 +414,11 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         // words; LABS_ENUM_LPW=8|16|32 forces a width (A/B timing)
         const char* lenv = std::getenv("LABS_ENUM_LPW");
         const int lwant = lenv ? std::atoi(lenv) : 0;
-        int lpw = P.S <= 32 ? 8 : (P.S <= 64 ? 16 : 32);
-        if (lwant == 32 || (lwant == 16 && P.S <= 64) || (lwant == 8 && P.S <= 32)) lpw = lwant;
+        // (4 lanes: eight chunks per warp share the per-step bookkeeping -- ctz, window
+        // addresses, the segment sum, the flip stores -- which costs as much as the lag work)
+        int lpw = P.S <= 32 ? 4 : (P.S <= 64 ? 16 : 32);
+        if (lwant == 32 || (lwant == 16 && P.S <= 64) || ((lwant == 8 || lwant == 4) && P.S <= 32))
+            lpw = lwant;
         const int segs = 32 / lpw;
         const size_t smem = static_cast<size_t>(4) * segs * P.warp_words * 4;
         int sms = 0;
@@ -419,7 +426,18 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         const uint64_t want = (P.nchunks + 4 * segs - 1) / (4 * segs);
         const int nj = (P.S + lpw - 1) / lpw;
         cudaEventRecord(e0, stream);
-        if (lpw == 8) {
+        if (lpw == 4) {
+            switch (nj) {
+                case 1: launch_enum<1, 4>(P, smem, stream, sms, want); break;
+                case 2: launch_enum<2, 4>(P, smem, stream, sms, want); break;
+                case 3: launch_enum<3, 4>(P, smem, stream, sms, want); break;
+                case 4: launch_enum<4, 4>(P, smem, stream, sms, want); break;
+                case 5: launch_enum<5, 4>(P, smem, stream, sms, want); break;
+                case 6: launch_enum<6, 4>(P, smem, stream, sms, want); break;
+                case 7: launch_enum<7, 4>(P, smem, stream, sms, want); break;
+                default: launch_enum<8, 4>(P, smem, stream, sms, want); break;
+            }
+        } else if (lpw == 8) {
             switch (nj) {
                 case 1: launch_enum<1, 8>(P, smem, stream, sms, want); break;
                 case 2: launch_enum<2, 8>(P, smem, stream, sms, want); break;
