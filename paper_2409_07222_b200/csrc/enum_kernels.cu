@@ -10,13 +10,13 @@
 //
 // Layout: 4 lanes (up to 32 lag words) -- eight chunks per warp -- or 16 / 32 lanes = one
 // chunk of 2^chunk_log2 consecutive g each (chunks from an atomic queue).
-// Lanes own the even lags t = 4(lane + 32j) + 1 .. +4 (C_{2t} in registers); the
-// sequence lives in shared memory as two parity byte arrays.  A step's energy change
-//     dE = sum_t dc_t (2 C_{2t} + dc_t),   dc_t = mul * (x_{a+2t} + x_{a-2t} - [t = k-a] x_b)
+// Lanes own the even lags t = 4(lane + LPW j) + 1 .. +4 (C_{2t} in registers); the
+// sequence lives in shared memory as two parity byte arrays.  A step updates every owned
+//     C_{2t} += dc_t,   dc_t = mul * (x_{a+2t} + x_{a-2t} - [t = k-a] x_b)
 // (mul = -4 x_a, or -2 x_a for the centre; the same fused even-lag rule as the walk
-// kernel's apply) is reduced per step with one REDUX (its result is consumed only after
-// 32 steps, off the critical path), lane s keeping step s's total; a lane scan then gives
-// every lane the energy of one configuration.  Exact integer arithmetic throughout.
+// kernel's apply; dc by two one-hot IDP4A) and accumulates the new C^2, so one segment sum
+// per step is the configuration's energy E = sum_t C_{2t}^2 (odd lags vanish); lane s of a
+// batch keeps step s's E.  Exact integer arithmetic throughout.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -156,7 +156,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     for (uint64_t s0 = 0; s0 < nmax; s0 += LPW) {
         const int nb = (int)(nsteps > s0 ? (nsteps - s0 < LPW ? nsteps - s0 : LPW) : 0);
         const int nbw = (int)(nmax - s0 < LPW ? nmax - s0 : LPW);
-        int mine = 0;  // dE of step s0 + sl
+        int mine = 0;  // E after step s0 + sl
         for (int s = 0; s < nbw; ++s) {  // (rolled: small code, no instruction-cache misses)
             const bool live = s < nb;
             const uint64_t i = s0 + s + 1;
@@ -176,25 +176,23 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             const uint32_t asB = sel4r((P.xoff + ah) & 3);
             const int tw = (tstar - 1) >> 2;
             const uint32_t tmask = ~(0xffu << (8 * ((tstar - 1) & 3)));
-            int acc = 0;
+            int acc = 0;  // sum of the owned C_{2t}^2 after the step: E = sum over lags
             const uint32_t mb = (uint32_t)mul & 0xffu;  // int8 mul: one-hot IDP4A selectors
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
+                // (lag words past the range read the zero padding: dc = 0, C stays 0)
                 const int sw = sl + LPW * j;
-                if (sw < P.S) {  // lanes past the lag range read nothing
-                    uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
-                    const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
-                    // the fused rule's [t = k-a] x_b term: the forward byte at t* is x_b
-                    if (sw == tw) fw &= tmask;
+                uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
+                const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
+                // the fused rule's [t = k-a] x_b term: the forward byte at t* is x_b
+                if (sw == tw) fw &= tmask;
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        // dc = mul (x_{a+2t} + x_{a-2t}): two IDP4A against mul e_b, no
-                        // byte unpacking (0 beyond k)
-                        const int e = (int)(mb << (8 * b));
-                        const int dc = __dp4a((int)fw, e, __dp4a((int)bw, e, 0));
-                        acc += dc * (2 * C[j][b] + dc);
-                        C[j][b] += dc;
-                    }
+                for (int b = 0; b < 4; ++b) {
+                    // dc = mul (x_{a+2t} + x_{a-2t}): two IDP4A against mul e_b, no byte
+                    // unpacking (0 beyond k)
+                    const int e = (int)(mb << (8 * b));
+                    C[j][b] += __dp4a((int)fw, e, __dp4a((int)bw, e, 0));
+                    acc += C[j][b] * C[j][b];
                 }
             }
             const int tot = seg_sum(acc);
@@ -204,14 +202,8 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             if (live && sl == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
             __syncwarp();
         }
-        int e = mine;  // dE of step s0 + sl
-#pragma unroll
-        for (int o = 1; o < LPW; o <<= 1) {
-            const int y = __shfl_up_sync(FULLMASK, e, o, LPW);
-            if (sl >= o) e += y;
-        }
         const bool vstep = sl < nb;
-        const int e_mine = energy + e;
+        const int e_mine = mine;
         const uint64_t g_mine = g0 + 1 + s0 + sl;
         const int e_last = __shfl_sync(FULLMASK, e_mine, nb > 0 ? nb - 1 : 0, LPW);
         if (nb > 0) energy = e_last;
@@ -356,12 +348,13 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
     P.m = m;
     P.nj = (P.k + 127) / 128;
     P.nwx = (kp1 + 3) / 4;
-    // window reads reach S+1 words past any position on both sides (lanes with 4-lag
-    // word sw < S only); the correlation prologue reads up to nwx + S + 1 words
+    // window reads reach SW+1 words past any position on both sides, SW = the lanes' lag
+    // words (up to S + 32: lanes past the lag range read zeros instead of branching); the
+    // correlation prologue reads up to nwx + S + 1 words
     const int S = (P.k + 3) / 4;
     P.S = S;
-    P.xoff = 4 * S + 16;
-    P.xwords = ((P.xoff + 4 * P.nwx + 4 * S + 32) / 4 + 3) & ~3;
+    P.xoff = 4 * (S + 32) + 16;
+    P.xwords = ((P.xoff + 4 * P.nwx + 4 * (S + 32) + 32) / 4 + 3) & ~3;
     P.warp_words = 2 * P.xwords;
     const uint64_t range = g_end - g_begin;
     int cl = chunk_log2 > 0 ? chunk_log2 : 12;
