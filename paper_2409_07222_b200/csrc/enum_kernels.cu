@@ -176,7 +176,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             const uint32_t asB = sel4r((P.xoff + ah) & 3);
             const int tw = (tstar - 1) >> 2;
             const uint32_t tmask = ~(0xffu << (8 * ((tstar - 1) & 3)));
-            int acc = 0;  // sum of the owned C_{2t}^2 after the step: E = sum over lags
+            int acc[4] = {0, 0, 0, 0};  // owned C_{2t}^2 after the step (four short chains)
             const uint32_t mb = (uint32_t)mul & 0xffu;  // int8 mul: one-hot IDP4A selectors
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
@@ -192,10 +192,10 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
                     // unpacking (0 beyond k)
                     const int e = (int)(mb << (8 * b));
                     C[j][b] += __dp4a((int)fw, e, __dp4a((int)bw, e, 0));
-                    acc += C[j][b] * C[j][b];
+                    acc[b] += C[j][b] * C[j][b];
                 }
             }
-            const int tot = seg_sum(acc);
+            const int tot = seg_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
             if (sl == s) mine = tot;
             __syncwarp();
             if (live && sl == 0) Xa[ah] = (int8_t)(-xa);
