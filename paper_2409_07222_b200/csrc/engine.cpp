@@ -255,7 +255,7 @@ constexpr double kBatchTargetMs = 100.0;     // coupled pools: one batch runs ab
 // of about kBatchTargetMs (sized from the measured walk rate, and from the remaining time
 // budget), two in flight; the stop conditions are evaluated in delivery order between
 // walks, exactly where the reference checks them, and a stop cancels the batches still
-// running.  With threads <= 1 the batches follow the --threads 1 order exactly (walker 0's
+// running (at the deadline, the batches not yet being replayed).  With threads <= 1 the batches follow the --threads 1 order exactly (walker 0's
 // restarts first; with unlimited restarts that is walker 0 alone, as in the reference).
 // With threads > 1 every walker runs concurrently, as the reference's pool does when
 // threads >= walkers (saw.cpp:242-257): each batch gives every unfinished walker its next
@@ -348,6 +348,7 @@ private:
     double ms_per_walk_ = 0;       // measured device time per walk at full residency
     double replay_ms_per_walk_ = 0;  // measured host replay time per walk (coupled pools)
     double wait_ms_ = 0;             // time the replay spent waiting for the devices
+    double wall_ms_per_walk_ = 0;    // consume wall time per walk of the latest batch
     int64_t last_batch_ = 1;         // walks of the latest coupled batch
     const bool timing_ = std::getenv("LABS_TIMING") != nullptr;
     // independent pools: per device, the next walk of its job list
@@ -483,6 +484,9 @@ private:
                 n = std::max<int64_t>(resident_all, static_cast<int64_t>(ngpu_ * target / ms_per_walk_));
                 if (replay_ms_per_walk_ > 0)
                     n = std::min<int64_t>(n, static_cast<int64_t>(target / replay_ms_per_walk_));
+                // the whole pipeline's pace (device, job post-processing, replay) per walk
+                if (wall_ms_per_walk_ > 0)
+                    n = std::min<int64_t>(n, static_cast<int64_t>(target / wall_ms_per_walk_));
                 n = std::max<int64_t>(1, std::min<int64_t>(n, 4 * last_batch_));
             }
             n = std::min<int64_t>(n, kMaxBatchWalks * ngpu_);
@@ -504,16 +508,23 @@ private:
                     ex_[static_cast<size_t>(g)]->push(std::move(jobs[static_cast<size_t>(g)]));
             if (timing_)
                 std::fprintf(stderr, "[labs] t=%.1f ms issue batch of %lld walks (%zu segs; device %.4f, "
-                             "replay %.4f ms/walk)\n",
+                             "replay %.4f, wall %.4f ms/walk)\n",
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count(),
-                             static_cast<long long>(last_batch_), segs.size(), ms_per_walk_, replay_ms_per_walk_);
+                             static_cast<long long>(last_batch_), segs.size(), ms_per_walk_, replay_ms_per_walk_,
+                             wall_ms_per_walk_);
             issued.push_back(std::move(idx));
             issued_segs.push_back(std::move(segs));
             return true;
         };
         while (issued.size() < 2 && issue()) {
         }
+        bool consumed_any = false;
         while (!issued.empty() && !stopped()) {
+            // at the deadline the batches whose replay has not begun are dropped (cancelled on
+            // the device): the reference starts no walk after its deadline (saw.cpp:204-208),
+            // and the overshoot stays one batch of replay
+            if (consumed_any && deadline_hit()) break;
+            consumed_any = true;
             const std::vector<size_t> idx = std::move(issued.front());
             const std::vector<Segment> segs = std::move(issued_segs.front());
             issued.pop_front();
@@ -524,11 +535,14 @@ private:
             for (size_t j = 0; j < segs.size() && !stopped(); ++j)
                 for (int64_t r = segs[j].r0; r < segs[j].r1 && !stopped(); ++r, ++nw)
                     deliver_next(idx[j], r);
-            // host replay time per walk (the waits for the devices excluded)
-            if (nw > 0)
-                replay_ms_per_walk_ = std::max(0.0, std::chrono::duration<double, std::milli>(
-                    std::chrono::steady_clock::now() - ta).count() - (wait_ms_ - wait0)) /
-                    static_cast<double>(nw);
+            // host replay time per walk (the waits for the devices excluded), and the batch's
+            // wall time per walk (waits included)
+            if (nw > 0) {
+                const double wall = std::chrono::duration<double, std::milli>(
+                    std::chrono::steady_clock::now() - ta).count();
+                replay_ms_per_walk_ = std::max(0.0, wall - (wait_ms_ - wait0)) / static_cast<double>(nw);
+                wall_ms_per_walk_ = wall / static_cast<double>(nw);
+            }
             while (issued.size() < 2 && issue()) {
             }
         }
