@@ -222,7 +222,7 @@ __device__ __forceinline__ void t_update_groups(const WalkParams& P, const uint3
             const int m = 8 * (grp >> 1) + 4 * (e & 1) + 2 * (grp & 1) + (e >> 1);
             const int vp = (e & 1) == APAR ? __dp4a((int)wx, (int)sx[e], 0) : 0;
             int v = __dp4a((int)wf, (int)sf[e], __dp4a((int)wg, (int)sg[e], vp));
-            if (m == mo) {
+            if ((e & 1) == APAR && m == mo) {  // (the pivot has a*'s parity)
                 v += vo;
                 xs[m] = -xs[m];
             }
@@ -345,6 +345,15 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     LABS_BC(P, kidx0 + 8 * P.nks - 4, 0, P.kwords);
     LABS_BC(P, xb, 0, cb == 0 ? P.xwords : P.xcw);
     LABS_BC(P, xb + 8 * P.nks - 4, 0, cb == 0 ? P.xwords : P.xcw);
+    // this lane's flip destination (lanes 0-7 at step (4)): copy c = sl & 3 of each parity,
+    // indexed by the half index's parity-array position i (byte xoff + i of the primary)
+    int8_t* flip0;
+    int8_t* flip1;
+    {
+        const int c = sl & 3;
+        flip0 = c == 0 ? w.X(0) + P.xoff : reinterpret_cast<int8_t*>(w.Xc(0, c)) + P.xoff - c - P.xcl;
+        flip1 = c == 0 ? w.X(1) + P.xoff : reinterpret_cast<int8_t*>(w.Xc(1, c)) + P.xoff - c - P.xcl;
+    }
     const bool one_key = L <= 1001;
     const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
@@ -650,14 +659,10 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         wide = wide_next;
         __syncwarp();
         // (4) write the flipped pair into the primary array and its three shifted copies
-        //     (lanes 0-3: x_a* in copy 0-3, lanes 4-7: x_b*), toggle the half bit (lane 8)
-        if (sl < 8 && !(cen && sl >= 4)) {
-            const int c = sl & 3;
-            const int pos = P.xoff + ((sl < 4) ? ah : (bstar >> 1));
-            int8_t* dst = c == 0 ? w.X(apar) + pos : reinterpret_cast<int8_t*>(w.Xc(apar, c)) + pos - c - P.xcl;
-            *dst = (int8_t)((sl < 4) ? -xa : -xb);
-        }
-        if (sl == 8) w.half[as >> 5] ^= 1u << (as & 31);
+        //     (lanes 0-3: x_a* in copy 0-3, lanes 4-7: x_b*).  (The packed half is not kept
+        //     up to date: a sieve hit rebuilds it from the parity arrays.)
+        if (sl < 8 && !(cen && sl >= 4))
+            (apar ? flip1 : flip0)[(sl < 4) ? ah : (bstar >> 1)] = (int8_t)((sl < 4) ? -xa : -xb);
         if (dbg) {
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj)
@@ -699,7 +704,13 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                     r[4] = (uint32_t)hf;
                     r[5] = (uint32_t)(hf >> 32);
                 }
-                for (int i = sl; i < P.hw; i += LPW) r[kRecHeader + i] = w.half[i];
+                // packed half: bit i <=> x_i = +1, x_i = X_{i&1}[i>>1] (one ballot per word)
+                for (int wd = 0; wd < P.hw; ++wd) {
+                    const int i = 32 * wd + sl;
+                    const bool plus = i < kp1 && w.X(i & 1)[P.xoff + (i >> 1)] > 0;
+                    const uint32_t word = __ballot_sync(FULLMASK, plus);
+                    if (sl == 0) r[kRecHeader + wd] = word;
+                }
                 __threadfence();
             }
             __syncwarp();
