@@ -146,21 +146,16 @@ template <int NQ, int NKS>
 __device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int kidx0, int xb,
                                             const uint32_t* __restrict__ xc0,
                                             const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
-    int ac2[NQ][2][4];
+    // one accumulator chain per (q-tile, parity): with 20 walks per SM the MMA latency is
+    // hidden by the other warps, and the second chain's registers and merge are saved
     uint32_t w0[NQ][NKS + 2], w2[NQ][NKS + 2];  // a0 / a2 words of steps -2 .. NKS-1
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) {
+    for (int j = 0; j < NQ; ++j)
 #pragma unroll
         for (int s = -2; s < NKS; ++s) {
             w0[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s];
             w2[j][s + 2] = Kw[kidx0 - 32 * j + 8 * s + 4];
         }
-
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) ac2[j][p][i] = 0;
-    }
 #pragma unroll
     for (int s = 0; s < NKS; ++s) {
         const uint32_t b00 = xc0[xb + 8 * s], b01 = xc0[xb + 8 * s + 4];
@@ -168,21 +163,10 @@ __device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int
 #pragma unroll
         for (int j = 0; j < NQ; ++j) {
             const uint32_t a[4] = {w0[j][s + 2], w0[j][s], w2[j][s + 2], w2[j][s]};
-            if ((s & 1) == 0) {
-                mma_s8(acc[j][0], a, b00, b01);
-                mma_s8(acc[j][1], a, b10, b11);
-            } else {
-                mma_s8(ac2[j][0], a, b00, b01);
-                mma_s8(ac2[j][1], a, b10, b11);
-            }
+            mma_s8(acc[j][0], a, b00, b01);
+            mma_s8(acc[j][1], a, b10, b11);
         }
     }
-#pragma unroll
-    for (int j = 0; j < NQ; ++j)
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[j][p][i] += ac2[j][p][i];
 }
 
 template <int NQ>
