@@ -18,7 +18,7 @@ for r in rows[1:]:
 tot = sum(t for _, t in agg.values())
 tag = sys.argv[2] if len(sys.argv) > 2 else ""
 print(f"# {tag} launch list: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400`\n")
-print("Command: `python bench.py --steps 2 --warmup 1 --restarts 8 --no-cpu-baseline` (L=451, 8192 walks per")
+print("Command: `python bench.py --steps 2 --warmup 1 --restarts 8 --no-cpu-baseline --no-c2` (L=451, 8192 walks per")
 print("launch; the `k_*` launches are the in-run INT32/IDP4A/IMMA peak microbenchmarks).  Cold-cache")
 print("serialised times: compare shares, not absolutes.\n")
 print("| kernel | launches | total ms | share |\n|---|---|---|---|")
