@@ -137,6 +137,13 @@ inline void throw_status(int rc) {
     }
 }
 
+// Device setup ahead of run_saw_pool (labs_saw_prepare): keeps it out of a time budget.
+inline void prepare_saw_pool(const SawConfig& config) {
+    const labs_saw_config c = config.to_c();
+    const int rc = labs_saw_prepare(&c);
+    if (rc != LABS_OK) throw_status(rc);
+}
+
 inline PoolStats run_saw_pool(const SawConfig& config, CandidateSink& sink) {  // saw.cpp:218
     struct Ctx {
         CandidateSink* sink;

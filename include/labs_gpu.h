@@ -128,6 +128,14 @@ int labs_saw_pool_run(const labs_saw_config* cfg, labs_candidate_fn emit, void* 
 int labs_saw_pool_run_batched(const labs_saw_config* cfg, labs_candidate_batch_fn emit, void* user,
                               labs_pool_stats* stats);
 
+/* Optional: set up now what a labs_saw_pool_run with this config's geometry (length,
+ * prefix, T_i, Bloom size, devices) would set up on its first call -- CUDA context,
+ * kernel modules, device tables, record rings -- so that a later pool's time budget
+ * (time_budget_s) is spent searching.  The reference has no device to initialise
+ * (saw.cpp:218 starts its clock on a warm process); the labs CLI calls this before
+ * run_saw_pool. */
+int labs_saw_prepare(const labs_saw_config* cfg);
+
 /* Derived configuration (saw.cpp:44-63, sequence.cpp:36-40, bloom.cpp:15-24). */
 typedef struct labs_saw_derived {
     int32_t prefix_len;

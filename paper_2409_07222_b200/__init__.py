@@ -36,6 +36,7 @@ from .api import (  # noqa: F401
     merit_factor,
     pq_score,
     rank_prefixes,
+    prepare_saw_pool,
     run_saw_pool,
     saw_walks,
     skew_flip_deltas,
@@ -46,5 +47,5 @@ __all__ = [
     "SawConfig", "WalkResult", "bench_plan", "canonical_hash", "rank_prefixes", "derive", "device_count",
     "energy_threshold_for_merit", "enumerate_class", "expand_skew", "format_record",
     "hex_encode", "imma_peak", "int32_peak", "library_path", "load_library", "merit_factor", "pq_score",
-    "run_saw_pool", "saw_walks", "skew_flip_deltas",
+    "prepare_saw_pool", "run_saw_pool", "saw_walks", "skew_flip_deltas",
 ]

@@ -140,6 +140,7 @@ def load_library():
         lib.labs_saw_pool_run_batched.argtypes = [C.POINTER(_Config), _BATCH_FN, C.c_void_p,
                                                   C.POINTER(_PoolStats)]
         lib.labs_saw_derive.argtypes = [C.POINTER(_Config), C.POINTER(_Derived)]
+        lib.labs_saw_prepare.argtypes = [C.POINTER(_Config)]
         lib.labs_saw_walks.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double,
                                        C.POINTER(C.c_int8), C.c_int64, C.c_int32, C.c_int32,
                                        C.POINTER(_WalkResult), _REC_FN, C.c_void_p]
@@ -374,6 +375,13 @@ def derive(cfg: SawConfig) -> dict:
     d = _Derived()
     _check(lib.labs_saw_derive(C.byref(cfg._c()), C.byref(d)))
     return {n: getattr(d, n) for n, _ in _Derived._fields_}
+
+
+def prepare_saw_pool(cfg: SawConfig) -> None:
+    """Set up the device state run_saw_pool(cfg) would create on its first call (CUDA
+    context, kernel modules, tables, rings) so that a later time budget is spent searching
+    (labs_saw_prepare)."""
+    _check(load_library().labs_saw_prepare(C.byref(cfg._c())))
 
 
 def run_saw_pool(cfg: SawConfig, sink: Optional[CandidateSink] = None) -> PoolStats:

@@ -186,7 +186,7 @@ struct SinkChain {
         const size_t n = b_energy.size();
         b_signs.resize(n * static_cast<size_t>(L));
         const size_t nthreads = std::min<size_t>(
-            n / 1024, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+            n / 256, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
         if (nthreads <= 1) {
             expand_range(0, n);
         } else {
@@ -237,8 +237,10 @@ std::vector<uint32_t> walker_list(const labs_saw_config& cfg, const Derived& d, 
 }
 
 constexpr int64_t kMaxBatchWalks = 1 << 20;  // walks per job (bounds the slot buffers)
-constexpr int64_t kPipelineBatches = 8;      // independent pools: jobs per device (>= 2 waves each)
+constexpr int64_t kPipelineBatches = 16;     // independent pools: jobs per device (>= 2 waves each)
 constexpr int64_t kQueueDepth = 3;           // jobs queued per device ahead of the replay
+constexpr int64_t kPreseedMaxWalks = 1 << 22;  // independent pools up to this many walks are
+                                               // seeded in one K3 launch (<= 512 MB of halves)
 constexpr double kBatchTargetMs = 100.0;     // coupled pools: one batch runs about this long
 
 // One run_saw_pool call.
@@ -294,6 +296,9 @@ public:
             ex_.emplace_back(new Executor(*r));
             ex_.back()->start();
         }
+        if (timing_)
+            std::fprintf(stderr, "[labs] pool t=%.2f ms: runners ready\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count());
         cur_.resize(static_cast<size_t>(ngpu));
         dev_kernel_ms_.assign(static_cast<size_t>(ngpu), 0.0);
         dev_seed_ms_.assign(static_cast<size_t>(ngpu), 0.0);
@@ -316,7 +321,6 @@ public:
         for (auto& e : ex_) e->stop();
         sink_.flush();  // before the jobs' record buffers are released
         cur_.clear();
-        retired_.clear();
         ex_.clear();
         if (!failed) release_runners(runners_);
         runners_.clear();
@@ -343,7 +347,6 @@ private:
         int64_t i = 0;
     };
     std::vector<Cursor> cur_;
-    std::vector<JobOut> retired_;  // replayed jobs whose records the sink may still reference
     std::vector<double> dev_kernel_ms_, dev_seed_ms_;
     double ms_per_walk_ = 0;       // measured device time per walk at full residency
     double replay_ms_per_walk_ = 0;  // measured host replay time per walk (coupled pools)
@@ -355,6 +358,8 @@ private:
     struct Gen {
         size_t k = 0;   // index into dev_walkers_[g]
         int64_t r = 0;
+        int64_t off = 0;      // walks handed out so far (= offset into the preseeded halves)
+        bool pre = false;     // the device's pool was preseeded
     };
     std::vector<Gen> feed_;
     std::vector<int64_t> chunk_;
@@ -387,6 +392,7 @@ private:
             const int64_t chunk = chunk_[static_cast<size_t>(g)];
             while (e.pushed() - e.popped() < kQueueDepth && f.k < wl.size()) {
                 Job job;
+                if (f.pre) job.pool_off = f.off;
                 while (job.nwalks < chunk && f.k < wl.size()) {
                     const int64_t take = std::min(R - f.r, chunk - job.nwalks);
                     job.segs.push_back(seg(wl[f.k], f.r, f.r + take));
@@ -397,6 +403,7 @@ private:
                         f.r = 0;
                     }
                 }
+                f.off += job.nwalks;
                 e.push(std::move(job));
             }
         }
@@ -413,6 +420,18 @@ private:
             const int64_t resident = runners_[static_cast<size_t>(g)]->resident;
             chunk_[static_cast<size_t>(g)] = std::max<int64_t>(1, std::min<int64_t>(
                 kMaxBatchWalks, nb == 1 ? total : std::max<int64_t>(2 * resident, (total + nb - 1) / nb)));
+        }
+        // one K3 launch seeds each device's whole pool before the first job (a per-job K3
+        // would wait at every job boundary for the other slot's walk blocks to free an SM)
+        for (int g = 0; g < ngpu_; ++g) {
+            const auto& wl = dev_walkers_[static_cast<size_t>(g)];
+            const int64_t total = static_cast<int64_t>(wl.size()) * R;
+            if (total <= 0 || total > kPreseedMaxWalks) continue;
+            std::vector<Segment> segs;
+            segs.reserve(wl.size());
+            for (size_t wi : wl) segs.push_back(seg(wi, 0, R));
+            runners_[static_cast<size_t>(g)]->preseed(segs, total);
+            feed_[static_cast<size_t>(g)].pre = true;
         }
         top_up();
         for (size_t wi = 0; wi < walkers_.size() && !stopped(); ++wi)
@@ -554,7 +573,9 @@ private:
         Cursor& c = cur_[static_cast<size_t>(g)];
         while (!c.have || c.i >= static_cast<int64_t>(c.job.walk_walker.size())) {
             if (c.have) {
-                retired_.push_back(std::move(c.job));
+                // the job is replayed: hand its candidates to the sink now, while the
+                // devices still run (only the last job's flush is left after the last kernel)
+                sink_.flush();
                 c.have = false;
             }
             top_up();
@@ -564,10 +585,6 @@ private:
             c.have = true;
             c.i = 0;
             account(g, c.job);
-            if (retired_.size() >= 2) {
-                sink_.flush();
-                retired_.clear();
-            }
         }
         const int64_t i = c.i++;
         const JobOut& b = c.job;
@@ -645,11 +662,21 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
     sink.emit = emit;
     sink.emit_batch = emit_batch;
     sink.user = user;
+    const bool timing = std::getenv("LABS_TIMING") != nullptr;
+    const auto mark = [&](const char* what) {
+        if (timing)
+            std::fprintf(stderr, "[labs] pool t=%.2f ms: %s\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                         what);
+    };
+    mark("configured");
     if (!walkers.empty()) {
         Pool pool(cfg, d, wp, sink, acc);
         try {
             pool.run(first, ndev_use, ngpu, walkers, t0);
+            mark("replayed");
             pool.shutdown(false);
+            mark("shut down");
         } catch (const CudaFailure& e) {
             pool.shutdown(true);
             set_error(e.what());
@@ -665,6 +692,7 @@ int pool_run(const labs_saw_config& cfg, labs_candidate_fn emit, labs_candidate_
         return LABS_ELOGIC;
     }
     sink.flush();
+    mark("flushed");
     acc.st.emitted = sink.emitted;
     acc.st.best_energy = acc.best_set ? acc.st.best_energy : 0;
     acc.st.delta_evals = cfg.count_visited ? acc.st.delta_evals : -1;
@@ -875,6 +903,37 @@ int labs_saw_pool_run(const labs_saw_config* cfg, labs_candidate_fn emit, void* 
         return LABS_EINVAL;
     }
     return pool_run(*cfg, emit, nullptr, user, stats);
+}
+
+int labs_saw_prepare(const labs_saw_config* cfg) {
+    if (!cfg) {
+        set_error("null config");
+        return LABS_EINVAL;
+    }
+    Derived d;
+    std::string err = derive(*cfg, d);
+    WalkParams wp;
+    if (err.empty()) err = walk_params_for(d, cfg->count_visited != 0, cfg->debug_check_energy != 0, wp);
+    if (!err.empty()) {
+        set_error(err);
+        return LABS_EINVAL;
+    }
+    const int ndev_avail = device_count();
+    const int first = std::max(0, cfg->device);
+    if (ndev_avail <= 0 || first >= ndev_avail) {
+        set_error("no CUDA device available (the Step-1 engine has no CPU fallback)");
+        return LABS_ENODEV;
+    }
+    const int ndev_use = std::max(1, ndev_avail - first);
+    std::vector<std::unique_ptr<DeviceRunner>> rs;
+    try {
+        for (int g = 0; g < std::max(1, cfg->n_gpus); ++g) rs.push_back(acquire_runner(first + g % ndev_use, wp));
+    } catch (const CudaFailure& e) {
+        set_error(e.what());
+        return LABS_ECUDA;
+    }
+    release_runners(rs);  // (the next pool with this geometry takes them from the pool)
+    return LABS_OK;
 }
 
 int labs_saw_pool_run_batched(const labs_saw_config* cfg, labs_candidate_batch_fn emit, void* user,

@@ -12,6 +12,7 @@ namespace labs_b200 {
 cudaError_t launch_saw_walk(const WalkParams& P, int grid, cudaStream_t st, int* score_out,
                             int* corr_out);
 cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st);
+cudaError_t preload_saw_seed();
 int walk_blocks_per_sm(WalkParams& P);  // (also places the fm table)
 size_t walk_smem_bytes(const WalkParams& P);
 
@@ -56,6 +57,8 @@ DeviceRunner::~DeviceRunner() {
             if (e) cudaEventDestroy(e);
         if (S.st) cudaStreamDestroy(S.st);
     }
+    for (cudaEvent_t e : {pre_ev0_, preseed_ev_})
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(drain_st_);
 }
 
@@ -69,6 +72,8 @@ void DeviceRunner::init(int device, const WalkParams& params) {
         for (cudaEvent_t* e : {&S.ev_s0, &S.ev_s1, &S.ev_k0, &S.ev_k1, &S.ev_done})
             LABS_CUDA(cudaEventCreate(e));
     }
+    LABS_CUDA(cudaEventCreate(&pre_ev0_));
+    LABS_CUDA(cudaEventCreate(&preseed_ev_));
     const auto& tt = TabTables::get();
     const int kp1 = wp.kp1, L = wp.L;
     std::vector<uint64_t> hfm(3 * static_cast<size_t>(kp1));
@@ -103,7 +108,8 @@ void DeviceRunner::init(int device, const WalkParams& params) {
     wp.salt_full = tt.salt[0][L];
     int sms = 0;
     LABS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int bps = std::max(1, walk_blocks_per_sm(wp));
+    const int bps = std::max(1, walk_blocks_per_sm(wp));  // (loads the walk kernel's module)
+    LABS_CUDA(preload_saw_seed());
     grid_cap = sms * bps;
     resident = static_cast<int64_t>(grid_cap) * wp.walks_per_block;
     if (std::getenv("LABS_TIMING"))
@@ -134,14 +140,11 @@ bool DeviceRunner::fits(int s, const Job& job) const {
     const size_t nw = static_cast<size_t>(std::max<int64_t>(job.nwalks, 1));
     const size_t nseg = job.segs.size();
     if (ring_slots_from_env() != ring_slots) return false;
-    if (nw * wp.hw > S.halves.n || nw * kWalkStatWords > S.stats.n ||
-        nw * kWalkStatWords > S.h_stats.n)
-        return false;
+    if (nw * kWalkStatWords > S.stats.n || nw * kWalkStatWords > S.h_stats.n) return false;
+    if (job.pool_off >= 0) return true;  // (halves from the pool buffer)
+    if (nw * wp.hw > S.halves.n) return false;
     if (job.host_halves && nw * wp.hw > S.h_halves.n) return false;
-    if (!job.host_halves && nseg > 0 &&
-        (3 * nseg > S.seg32.n || 2 * nseg > S.seg64.n || nseg > S.seg_init.n ||
-         3 * nseg > S.h_seg32.n || 2 * nseg > S.h_seg64.n || nseg > S.h_init.n))
-        return false;
+    if (!job.host_halves && nseg > 0 && !S.sb.fits(nseg)) return false;
     return true;
 }
 
@@ -168,17 +171,11 @@ void DeviceRunner::launch(int s, const Job& job) {
     // sized for the job: the next one then launches without waiting)
     for (Slot& T : slot_) {
         if (&T != &S && T.busy) continue;
-        T.halves.reserve(static_cast<size_t>(std::max<int64_t>(nw, 1)) * wp.hw);
         T.stats.reserve(static_cast<size_t>(std::max<int64_t>(nw, 1)) * kWalkStatWords);
         T.h_stats.reserve(static_cast<size_t>(std::max<int64_t>(nw, 1)) * kWalkStatWords);
-        if (!job.host_halves && nseg > 0) {
-            T.h_seg32.reserve(3 * static_cast<size_t>(nseg));
-            T.h_seg64.reserve(2 * static_cast<size_t>(nseg));
-            T.h_init.reserve(static_cast<size_t>(nseg));
-            T.seg32.reserve(3 * static_cast<size_t>(nseg));
-            T.seg64.reserve(2 * static_cast<size_t>(nseg));
-            T.seg_init.reserve(static_cast<size_t>(nseg));
-        }
+        if (job.pool_off >= 0) continue;
+        T.halves.reserve(static_cast<size_t>(std::max<int64_t>(nw, 1)) * wp.hw);
+        if (!job.host_halves && nseg > 0) T.sb.reserve(static_cast<size_t>(nseg));
     }
     S.seeded = false;
     const int64_t want_slots = ring_slots_from_env();  // (tests shrink it per call)
@@ -200,52 +197,27 @@ void DeviceRunner::launch(int s, const Job& job) {
         std::memcpy(S.h_halves.p, job.host_halves, words * 4);
         LABS_CUDA(cudaMemcpyAsync(S.halves.p, S.h_halves.p, words * 4, cudaMemcpyHostToDevice, S.st));
         S.out.h2d += static_cast<int64_t>(words) * 4;
-    } else if (nseg > 0) {
-        // K3 job tables: walker, prefix bits, generator slot | restarts, first walk | init
-        int64_t off = 0;
-        for (int i = 0; i < nseg; ++i) {
-            const Segment& g = job.segs[static_cast<size_t>(i)];
-            S.h_seg32.p[i] = g.walker;
-            S.h_seg32.p[nseg + i] = d->prefix_bits[g.walker % static_cast<uint32_t>(d->nprefix)];
-            S.h_seg32.p[2 * nseg + i] = g.gen;
-            S.h_seg64.p[i] = g.r1 - g.r0;
-            S.h_seg64.p[nseg + i] = off;
-            S.h_init.p[i] = g.r0 == 0 ? 1 : 0;
-            off += g.r1 - g.r0;
+    } else if (job.pool_off >= 0) {
+        if (job.pool_off + nw > pool_walks_) throw CudaFailure("job outside the preseeded pool");
+        LABS_CUDA(cudaStreamWaitEvent(S.st, preseed_ev_, 0));
+        S.out.h2d += pending_h2d_;
+        pending_h2d_ = 0;
+        if (!preseed_timed_) {  // (the preseed's K3 time is reported with the first job)
+            S.seeded = true;
+            S.seed_from = pre_ev0_;
+            S.seed_to = preseed_ev_;
+            preseed_timed_ = true;
         }
-        LABS_CUDA(cudaMemcpyAsync(S.seg32.p, S.h_seg32.p, 12 * static_cast<size_t>(nseg),
-                                  cudaMemcpyHostToDevice, S.st));
-        LABS_CUDA(cudaMemcpyAsync(S.seg64.p, S.h_seg64.p, 16 * static_cast<size_t>(nseg),
-                                  cudaMemcpyHostToDevice, S.st));
-        LABS_CUDA(cudaMemcpyAsync(S.seg_init.p, S.h_init.p, 4 * static_cast<size_t>(nseg),
-                                  cudaMemcpyHostToDevice, S.st));
-        S.out.h2d += 32 * static_cast<int64_t>(nseg);
-        SeedParams sp{};
-        sp.kp1 = wp.kp1;
-        sp.p = wp.p;
-        sp.hw = wp.hw;
-        sp.nseg = nseg;
-        sp.seed = seed;
-        sp.walker_ids = S.seg32.p;
-        sp.prefix_bits = S.seg32.p + nseg;
-        sp.seg_slot = S.seg32.p + 2 * nseg;
-        sp.seg_restarts = S.seg64.p;
-        sp.seg_offset = S.seg64.p + nseg;
-        sp.seg_init = S.seg_init.p;
-        sp.rng_state = rng.p;
-        sp.halves = S.halves.p;
-        // generator streams continue across jobs: K3 launches run in job order
-        if (last_seed_) LABS_CUDA(cudaStreamWaitEvent(S.st, last_seed_, 0));
-        LABS_CUDA(cudaEventRecord(S.ev_s0, S.st));
-        LABS_CUDA(launch_saw_seed(sp, S.st));
-        LABS_CUDA(cudaEventRecord(S.ev_s1, S.st));
-        last_seed_ = S.ev_s1;
+    } else if (nseg > 0) {
+        S.out.h2d += seed_into(S.st, S.sb, job.segs, S.halves.p, S.ev_s0, S.ev_s1);
         S.seeded = true;
+        S.seed_from = S.ev_s0;
+        S.seed_to = S.ev_s1;
     }
     LABS_CUDA(cudaMemsetAsync(S.ctr.p, 0, 4 * sizeof(unsigned long long), S.st));
     WalkParams P = wp;
     P.nwalks = nw;
-    P.halves = S.halves.p;
+    P.halves = job.pool_off >= 0 ? pool_halves.p + job.pool_off * wp.hw : S.halves.p;
     P.rec = S.ring.p;
     P.rec_tag = S.tag.p;
     P.rec_seq0 = S.seq0;
@@ -272,6 +244,59 @@ void DeviceRunner::launch(int s, const Job& job) {
     S.tail = 0;
     S.cancel_sent = false;
     S.busy = true;
+}
+
+int64_t DeviceRunner::seed_into(cudaStream_t st, SeedBufs& B, const std::vector<Segment>& segs,
+                                uint32_t* halves, cudaEvent_t ev0, cudaEvent_t ev1) {
+    const int nseg = static_cast<int>(segs.size());
+    int64_t off = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const Segment& g = segs[static_cast<size_t>(i)];
+        B.h_seg32.p[i] = g.walker;
+        B.h_seg32.p[nseg + i] = d->prefix_bits[g.walker % static_cast<uint32_t>(d->nprefix)];
+        B.h_seg32.p[2 * nseg + i] = g.gen;
+        B.h_seg64.p[i] = g.r1 - g.r0;
+        B.h_seg64.p[nseg + i] = off;
+        B.h_init.p[i] = g.r0 == 0 ? 1 : 0;
+        off += g.r1 - g.r0;
+    }
+    LABS_CUDA(cudaMemcpyAsync(B.seg32.p, B.h_seg32.p, 12 * static_cast<size_t>(nseg),
+                              cudaMemcpyHostToDevice, st));
+    LABS_CUDA(cudaMemcpyAsync(B.seg64.p, B.h_seg64.p, 16 * static_cast<size_t>(nseg),
+                              cudaMemcpyHostToDevice, st));
+    LABS_CUDA(cudaMemcpyAsync(B.seg_init.p, B.h_init.p, 4 * static_cast<size_t>(nseg),
+                              cudaMemcpyHostToDevice, st));
+    SeedParams sp{};
+    sp.kp1 = wp.kp1;
+    sp.p = wp.p;
+    sp.hw = wp.hw;
+    sp.nseg = nseg;
+    sp.seed = seed;
+    sp.walker_ids = B.seg32.p;
+    sp.prefix_bits = B.seg32.p + nseg;
+    sp.seg_slot = B.seg32.p + 2 * nseg;
+    sp.seg_restarts = B.seg64.p;
+    sp.seg_offset = B.seg64.p + nseg;
+    sp.seg_init = B.seg_init.p;
+    sp.rng_state = rng.p;
+    sp.halves = halves;
+    // generator streams continue across jobs: K3 launches run in job order
+    if (last_seed_) LABS_CUDA(cudaStreamWaitEvent(st, last_seed_, 0));
+    LABS_CUDA(cudaEventRecord(ev0, st));
+    LABS_CUDA(launch_saw_seed(sp, st));
+    LABS_CUDA(cudaEventRecord(ev1, st));
+    last_seed_ = ev1;
+    return 32 * static_cast<int64_t>(nseg);
+}
+
+void DeviceRunner::preseed(const std::vector<Segment>& segs, int64_t nwalks) {
+    for (const Slot& S : slot_)
+        if (S.busy) throw CudaFailure("preseed on a busy runner");
+    pool_halves.reserve(static_cast<size_t>(std::max<int64_t>(nwalks, 1)) * wp.hw);
+    pool_sb.reserve(std::max<size_t>(segs.size(), 1));
+    pending_h2d_ += seed_into(slot_[0].st, pool_sb, segs, pool_halves.p, pre_ev0_, preseed_ev_);
+    pool_walks_ = nwalks;
+    preseed_timed_ = false;
 }
 
 bool DeviceRunner::done(int s) {
@@ -370,7 +395,7 @@ JobOut DeviceRunner::finish(int s) {
     LABS_CUDA(cudaEventElapsedTime(&ms, S.ev_k0, S.ev_k1));
     out.kernel_ms = ms;
     if (S.seeded) {
-        LABS_CUDA(cudaEventElapsedTime(&ms, S.ev_s0, S.ev_s1));
+        LABS_CUDA(cudaEventElapsedTime(&ms, S.seed_from, S.seed_to));
         out.seed_ms = ms;
     }
     if (!out.cancelled) out.group(wp.rec_words);
@@ -464,7 +489,10 @@ void Executor::body() {
                 if (timing)
                     std::fprintf(stderr, "[labs] dev %d t=%.2f ms launch %lld walks on slot %d\n", dr_.dev,
                                  ms(), static_cast<long long>(job.nwalks), s);
+                const double tl = ms();
                 dr_.launch(s, job);
+                if (timing && ms() - tl > 1.0)
+                    std::fprintf(stderr, "[labs] dev %d launch call took %.2f ms\n", dr_.dev, ms() - tl);
                 inflight.push_back(s);
                 continue;
             }
@@ -472,7 +500,10 @@ void Executor::body() {
                 for (int s : inflight) dr_.cancel(s);
             const int s0 = inflight.front();
             if (dr_.done(s0)) {
+                const double tf = ms();
                 JobOut o = dr_.finish(s0);
+                if (timing && ms() - tf > 1.0)
+                    std::fprintf(stderr, "[labs] dev %d finish call took %.2f ms\n", dr_.dev, ms() - tf);
                 if (timing)
                     std::fprintf(stderr, "[labs] dev %d t=%.2f ms done slot %d (kernel %.2f ms, seed %.2f ms, "
                                  "%lld records, %lld ring drains)\n", dr_.dev, ms(), s0, o.kernel_ms,
@@ -488,7 +519,10 @@ void Executor::body() {
             }
             const auto now = std::chrono::steady_clock::now();
             if (now - last_poll > std::chrono::microseconds(500)) {
+                const double tp = ms();
                 for (int s : inflight) dr_.poll(s);
+                if (timing && ms() - tp > 1.0)
+                    std::fprintf(stderr, "[labs] dev %d poll took %.2f ms\n", dr_.dev, ms() - tp);
                 last_poll = now;
             }
             std::this_thread::sleep_for(std::chrono::microseconds(20));

@@ -10,6 +10,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -48,8 +49,9 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
-    void reserve(size_t count) {  // grow-only; contents are not preserved
+    void reserve(size_t count) {  // grow-only (geometric); contents are not preserved
         if (count <= n) return;
+        count = std::max(count, 2 * n);  // (growing batches would reallocate every time)
         release();
         LABS_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
         n = count;
@@ -67,8 +69,9 @@ struct PinnedBuf {
     ~PinnedBuf() {
         if (p) cudaFreeHost(p);
     }
-    void reserve(size_t count) {
+    void reserve(size_t count) {  // grow-only (geometric)
         if (count <= n) return;
+        count = std::max(count, 2 * n);
         if (p) cudaFreeHost(p);
         p = nullptr;
         n = 0;
@@ -97,6 +100,9 @@ struct WalkRecordView {
 struct Job {
     std::vector<Segment> segs;
     int64_t nwalks = 0;
+    // >= 0: the walks' initial halves were seeded ahead (DeviceRunner::preseed) and start at
+    // this walk of the runner's pool buffer: no K3 in this job's launch
+    int64_t pool_off = -1;
     // seed-table mode: packed initial halves (nwalks x hw) instead of K3
     const uint32_t* host_halves = nullptr;
     int* score_out = nullptr;  // labs_skew_flip_deltas: deltas / correlations of the start
@@ -117,6 +123,29 @@ struct JobOut {
     int64_t ring_drains = 0;               // partial drains while the launch ran
     bool cancelled = false;
     void group(int rec_words);
+};
+
+// K3 job tables (device + pinned staging): walker, prefix bits, generator slot | restarts,
+// first walk | fresh-stream flag, per segment.
+struct SeedBufs {
+    DevBuf<uint32_t> seg32;
+    DevBuf<int64_t> seg64;
+    DevBuf<int32_t> seg_init;
+    PinnedBuf<uint32_t> h_seg32;
+    PinnedBuf<int64_t> h_seg64;
+    PinnedBuf<int32_t> h_init;
+    bool fits(size_t nseg) const {
+        return 3 * nseg <= seg32.n && 2 * nseg <= seg64.n && nseg <= seg_init.n &&
+               3 * nseg <= h_seg32.n && 2 * nseg <= h_seg64.n && nseg <= h_init.n;
+    }
+    void reserve(size_t nseg) {
+        h_seg32.reserve(3 * nseg);
+        h_seg64.reserve(2 * nseg);
+        h_init.reserve(nseg);
+        seg32.reserve(3 * nseg);
+        seg64.reserve(2 * nseg);
+        seg_init.reserve(nseg);
+    }
 };
 
 class DeviceRunner {
@@ -142,6 +171,10 @@ public:
     void cancel(int s);                 // ask the slot's K1 to stop taking walks
     JobOut finish(int s);               // after done(s): final drain, stats, grouping
     JobOut run_sync(const Job& job);    // launch on slot 0 and wait (bench, seed-table mode)
+    // Seed the initial halves of a whole (independent) pool in one K3 launch, walks in
+    // `segs` order, before any job is pushed; jobs then take slices (Job::pool_off), so no
+    // K3 waits behind the other slot's walk blocks at a job boundary.  Idle runner only.
+    void preseed(const std::vector<Segment>& segs, int64_t nwalks);
     bool busy(int s) const { return slot_[s].busy; }
 
 private:
@@ -149,16 +182,16 @@ private:
         cudaStream_t st = nullptr;
         cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr,
                     ev_done = nullptr;
-        DevBuf<uint32_t> halves, ring, tag, seg32;  // seg32: walker, prefix bits, generator
-        DevBuf<int64_t> stats, seg64;               // seg64: restarts, first walk
-        DevBuf<int32_t> seg_init;
+        DevBuf<uint32_t> halves, ring, tag;
+        DevBuf<int64_t> stats;
         DevBuf<unsigned long long> ctr;             // head, walk queue, tail, ctl (2 x int)
-        PinnedBuf<uint32_t> h_seg32, h_ring, h_tag, h_halves;
-        PinnedBuf<int64_t> h_seg64, h_stats;
-        PinnedBuf<int32_t> h_init;
+        SeedBufs sb;
+        PinnedBuf<uint32_t> h_ring, h_tag, h_halves;
+        PinnedBuf<int64_t> h_stats;
         PinnedBuf<unsigned long long> h_ctr, h_head, h_tail;
         PinnedBuf<int> h_cancel;
         bool busy = false, seeded = false, cancel_sent = false;
+        cudaEvent_t seed_from = nullptr, seed_to = nullptr;  // this job's K3 (seed_ms)
         int64_t nwalks = 0;
         unsigned long long tail = 0;
         unsigned long long seq0 = 0;  // records this slot's ring carried in earlier launches
@@ -167,8 +200,17 @@ private:
     Slot slot_[2];
     cudaStream_t drain_st_ = nullptr;
     cudaEvent_t last_seed_ = nullptr;   // the latest K3 (the next one waits for it)
+    cudaEvent_t pre_ev0_ = nullptr, preseed_ev_ = nullptr;  // the pool's preseed K3 (pool_off
+                                                            // jobs wait for preseed_ev_)
     DevBuf<uint64_t> fm, tab, tabfull, rng;
+    DevBuf<uint32_t> pool_halves;       // preseeded halves of the current pool
+    SeedBufs pool_sb;
+    int64_t pool_walks_ = 0, pending_h2d_ = 0;
+    bool preseed_timed_ = true;
     void drain(Slot& S, unsigned long long head, bool final);
+    // K3 of `segs` into `halves` on stream st (after the previous K3); returns H2D bytes
+    int64_t seed_into(cudaStream_t st, SeedBufs& B, const std::vector<Segment>& segs,
+                      uint32_t* halves, cudaEvent_t ev0, cudaEvent_t ev1);
 };
 
 // One host thread per device: runs queued jobs two at a time on the runner's slots, keeps

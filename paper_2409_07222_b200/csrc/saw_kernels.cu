@@ -136,6 +136,12 @@ int walk_blocks_per_sm(WalkParams& P) {
     return n_l1;
 }
 
+// Load the seed kernel's module now (lazy loading would do it at the first job's launch).
+cudaError_t preload_saw_seed() {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, saw_seed_kernel);
+}
+
 cudaError_t launch_saw_seed(const SeedParams& P, cudaStream_t st) {
     const int bs = 128;
     const int grid = (P.nseg + bs - 1) / bs;

@@ -94,6 +94,7 @@ int cmd_saw(int argc, char** argv) {
         file = std::make_unique<FileSink>(v["--out"]);
         sink = file.get();
     }
+    labs_b200::prepare_saw_pool(saw);  // (device setup outside the --seconds budget)
     const auto stats = labs_b200::run_saw_pool(saw, *sink);
     std::cerr << "walks=" << stats.walks << " iterations=" << stats.iterations
               << " emitted=" << stats.emitted << " bestE=" << stats.best_energy

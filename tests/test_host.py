@@ -42,6 +42,8 @@ def test_no_cpu_fallback(labs):
         labs.run_saw_pool(labs.SawConfig(length=31, target_merit=3.0, max_restarts=1))
     with pytest.raises(labs.api.NoDevice):
         labs.skew_flip_deltas(31, np.ones((1, 16), np.int8))
+    with pytest.raises(labs.api.NoDevice):
+        labs.prepare_saw_pool(labs.SawConfig(length=31, target_merit=3.0, max_restarts=1))
 
 
 def test_host_helpers_match_oracle(labs, restated):
