@@ -423,7 +423,9 @@ private:
         }
         // one K3 launch seeds each device's whole pool before the first job (a per-job K3
         // would wait at every job boundary for the other slot's walk blocks to free an SM)
-        for (int g = 0; g < ngpu_; ++g) {
+        const char* pre_env = std::getenv("LABS_PRESEED");  // (A/B, tests: 0 = K3 per job)
+        const bool preseed = !(pre_env && std::string(pre_env) == "0");
+        for (int g = 0; g < ngpu_ && preseed; ++g) {
             const auto& wl = dev_walkers_[static_cast<size_t>(g)];
             const int64_t total = static_cast<int64_t>(wl.size()) * R;
             if (total <= 0 || total > kPreseedMaxWalks) continue;

@@ -718,11 +718,13 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     __syncwarp();
 }
 
-template <int NQ, bool COUNT>
+// FMS: the flip-mask table fm has a shared copy per block (P.fm_words > 0, when that costs
+// no resident block) -- a compile-time choice, so its reads are shared loads, not generic ones
+template <int NQ, bool COUNT, bool FMS>
 __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     const uint64_t* fm = P.fm;
-    if (P.fm_words) {
+    if (FMS || P.fm_words) {  // (FMS = false keeps the generic-pointer form: fewer registers)
         uint64_t* fs = reinterpret_cast<uint64_t*>(smem_u4);
         for (int i = threadIdx.x; i < 3 * P.kp1; i += blockDim.x) fs[i] = P.fm[i];
         __syncthreads();
@@ -755,7 +757,9 @@ __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma
 template <int NQ>
 cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
                             int* score_out, int* corr_out, bool count) {
-    auto kfn = count ? saw_walk_mma_kernel<NQ, true> : saw_walk_mma_kernel<NQ, false>;
+    const bool fms = P.fm_words > 0;
+    auto kfn = count ? (fms ? saw_walk_mma_kernel<NQ, true, true> : saw_walk_mma_kernel<NQ, true, false>)
+                     : (fms ? saw_walk_mma_kernel<NQ, false, true> : saw_walk_mma_kernel<NQ, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, P.warps_per_block * 32, smem, st>>>(P, score_out, corr_out);
@@ -765,10 +769,9 @@ cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStre
 template <int NQ>
 int blocks_per_sm_mma(const WalkParams& P, size_t smem) {
     int n = 0;
-    cudaFuncSetAttribute(saw_walk_mma_kernel<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, saw_walk_mma_kernel<NQ, false>,
-                                                      P.warps_per_block * 32, smem) != cudaSuccess)
+    auto kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, false, true> : saw_walk_mma_kernel<NQ, false, false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kfn, P.warps_per_block * 32, smem) != cudaSuccess)
         return 0;
     return n;
 }

@@ -45,9 +45,13 @@ def test_pipelined_jobs_equal_one_job(labs, reference, monkeypatch):
     monkeypatch.setenv("LABS_PIPELINE_BATCHES", "1")
     st1, got1 = _run(labs, **kw)
     monkeypatch.delenv("LABS_PIPELINE_BATCHES")
+    monkeypatch.setenv("LABS_PRESEED", "0")  # one K3 per job instead of one for the pool
+    st0, got0 = _run(labs, **kw)
+    monkeypatch.delenv("LABS_PRESEED")
     assert st.walks == 65536 and [_key(c) for c in got] == [_key(c) for c in got1]
+    assert [_key(c) for c in got] == [_key(c) for c in got0]
     for k in ("walks", "iterations", "emitted", "best_energy", "emitted_raw"):
-        assert getattr(st, k) == getattr(st1, k), k
+        assert getattr(st, k) == getattr(st1, k) == getattr(st0, k), k
     # walkers 1000..1023 (their restarts sit in the pipeline's last jobs)
     sub = dict(kw, walker_begin=1000)
     st2, got2 = _run(labs, **sub)
