@@ -113,7 +113,7 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     for (int j = 0; j < NJ; ++j) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int t = 4 * (sl + LPW * j) + 1 + b;
+            const int t = 4 * (sl * NJ + j) + 1 + b;
             int acc = 0;
             if (t <= k) {
                 const int dw = t >> 2;
@@ -167,31 +167,37 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             const uint32_t* Xaw = (a & 1) ? X1w : X0w;
             const int xa = Xa[ah];
             const bool cen = a == k;
-            const int tstar = cen ? -3 : k - a;  // (-3: matches no lag word)
             const int xb = ((k - a) & 1) ? -xa : xa;
             const int mul = live ? (cen ? -2 * xa : -4 * xa) : 0;
             const int awF = (P.xoff + ah + 1) >> 2;
             const uint32_t asF = sel4((P.xoff + ah + 1) & 3);
             const int awB = (P.xoff + ah - 4) >> 2;
             const uint32_t asB = sel4r((P.xoff + ah) & 3);
-            const int tw = (tstar - 1) >> 2;
-            const uint32_t tmask = ~(0xffu << (8 * ((tstar - 1) & 3)));
             int acc[4] = {0, 0, 0, 0};  // owned C_{2t}^2 after the step (four short chains)
             const uint32_t mb = (uint32_t)mul & 0xffu;  // int8 mul: one-hot IDP4A selectors
+            const int e1[4] = {(int)mb, (int)(mb << 8), (int)(mb << 16), (int)(mb << 24)};
+            // the fused rule's [t = k-a] x_b term: x_b is read once, by the forward window at
+            // t* = k-a, so it is zeroed in the array for this step (restored, flipped, below)
+            if (live && sl == 1 && !cen) Xa[(L - 1 - a) >> 1] = 0;
+            __syncwarp();
+            // the lane's lag words s0 .. s0+NJ-1 are consecutive: NJ+1 words per window side
+            // (lag words past the range read the zero padding: dc = 0, C stays 0)
+            const int s0w = sl * NJ;
+            uint32_t wf[NJ + 1], wb[NJ + 1];
+#pragma unroll
+            for (int q = 0; q <= NJ; ++q) {
+                wf[q] = Xaw[awF + s0w + q];
+                wb[q] = Xaw[awB - s0w + 1 - q];
+            }
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
-                // (lag words past the range read the zero padding: dc = 0, C stays 0)
-                const int sw = sl + LPW * j;
-                uint32_t fw = __byte_perm(Xaw[awF + sw], Xaw[awF + sw + 1], asF);
-                const uint32_t bw = __byte_perm(Xaw[awB - sw], Xaw[awB - sw + 1], asB);
-                // the fused rule's [t = k-a] x_b term: the forward byte at t* is x_b
-                if (sw == tw) fw &= tmask;
+                const uint32_t fw = __byte_perm(wf[j], wf[j + 1], asF);
+                const uint32_t bw = __byte_perm(wb[j + 1], wb[j], asB);
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    // dc = mul (x_{a+2t} + x_{a-2t}): two IDP4A against mul e_b, no byte
-                    // unpacking (0 beyond k)
-                    const int e = (int)(mb << (8 * b));
-                    C[j][b] += __dp4a((int)fw, e, __dp4a((int)bw, e, 0));
+                    // dc = mul (x_{a+2t} + x_{a-2t}): two IDP4A against mul e_b chained into
+                    // C, no byte unpacking (0 beyond k)
+                    C[j][b] = __dp4a((int)fw, e1[b], __dp4a((int)bw, e1[b], C[j][b]));
                     acc[b] += C[j][b] * C[j][b];
                 }
             }
