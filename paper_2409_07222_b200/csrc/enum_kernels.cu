@@ -153,6 +153,17 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
         const uint64_t other = __shfl_xor_sync(FULLMASK, (unsigned long long)nmax, o);
         nmax = other > nmax ? other : nmax;
     }
+    // The flip position of step i (1-based; idle steps: any valid position, no writes).
+    const auto flip_pos = [&](uint64_t i) {
+        const int tz = aligned ? __ffs((unsigned)i) - 1 : __ffsll((long long)(g0 + i)) - 1;
+        return i <= nsteps ? P.p + tz : P.p;
+    };
+    // The fused rule's [t = k-a] x_b term: x_b is read once, by the forward window at
+    // t* = k-a, so it is zero in the array during the step (written flipped after it).  The
+    // zero of step i+1 is stored with step i's flips: one warp barrier per step.
+    int a = flip_pos(1);
+    if (nsteps >= 1 && sl == 2 && a != k) ((a & 1) ? X1 : X0)[P.xoff + ((L - 1 - a) >> 1)] = 0;
+    __syncwarp();
     for (uint64_t s0 = 0; s0 < nmax; s0 += LPW) {
         const int nb = (int)(nsteps > s0 ? (nsteps - s0 < LPW ? nsteps - s0 : LPW) : 0);
         const int nbw = (int)(nmax - s0 < LPW ? nmax - s0 : LPW);
@@ -160,8 +171,6 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
         for (int s = 0; s < nbw; ++s) {  // (rolled: small code, no instruction-cache misses)
             const bool live = s < nb;
             const uint64_t i = s0 + s + 1;
-            const int tz = aligned ? __ffs((unsigned)i) - 1 : __ffsll((long long)(g0 + i)) - 1;
-            const int a = live ? P.p + tz : P.p;  // (idle: any valid position, no writes)
             const int ah = a >> 1;
             int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
             const uint32_t* Xaw = (a & 1) ? X1w : X0w;
@@ -176,10 +185,6 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             int acc[4] = {0, 0, 0, 0};  // owned C_{2t}^2 after the step (four short chains)
             const uint32_t mb = (uint32_t)mul & 0xffu;  // int8 mul: one-hot IDP4A selectors
             const int e1[4] = {(int)mb, (int)(mb << 8), (int)(mb << 16), (int)(mb << 24)};
-            // the fused rule's [t = k-a] x_b term: x_b is read once, by the forward window at
-            // t* = k-a, so it is zeroed in the array for this step (restored, flipped, below)
-            if (live && sl == 1 && !cen) Xa[(L - 1 - a) >> 1] = 0;
-            __syncwarp();
             // the lane's lag words s0 .. s0+NJ-1 are consecutive: NJ+1 words per window side
             // (lag words past the range read the zero padding: dc = 0, C stays 0)
             const int s0w = sl * NJ;
@@ -203,10 +208,16 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             }
             const int tot = seg_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
             if (sl == s) mine = tot;
+            // stores: lane 0 x_a -> -x_a, lane 1 x_b -> -x_b, lane 2 the next step's x_b -> 0
+            const int an = flip_pos(i + 1);
+            const bool st = sl == 0 ? live : (sl == 1 ? live && !cen : (sl == 2 && i < nsteps && an != k));
+            int8_t* dst = sl == 2 ? ((an & 1) ? X1 : X0) + P.xoff + ((L - 1 - an) >> 1)
+                                  : Xa + (sl == 0 ? ah : (L - 1 - a) >> 1);
+            const int8_t val = (int8_t)(sl == 0 ? -xa : (sl == 1 ? -xb : 0));
             __syncwarp();
-            if (live && sl == 0) Xa[ah] = (int8_t)(-xa);
-            if (live && sl == 1 && !cen) Xa[(L - 1 - a) >> 1] = (int8_t)(-xb);
+            if (st) *dst = val;
             __syncwarp();
+            a = an;
         }
         const bool vstep = sl < nb;
         const int e_mine = mine;
