@@ -32,7 +32,7 @@ namespace labs_b200 {
 
 #define FULLMASK 0xffffffffu
 #ifndef LABS_ENUM_MINB
-#define LABS_ENUM_MINB 5  // resident 128-thread blocks per SM the 4-lane variants target (93 registers)
+#define LABS_ENUM_MINB 6  // resident 128-thread blocks per SM the 4-lane variants target (<= 85 registers)
 #endif
 
 struct EnumLaunch {
@@ -146,31 +146,30 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
     // ctz(g0 + i) = ctz(i) when the chunk start is a multiple of 2^chunk_log2 (every chunk
     // when g_begin is aligned); else the 64-bit path.
     const bool aligned = (g0 & ((1ull << P.chunk_log2) - 1)) == 0;
-    const uint64_t nsteps = g1 - g0 - 1;
-    uint64_t nmax = nsteps;  // warp-uniform bound
+    const int nsteps = (int)(g1 - g0 - 1);  // (< 2^chunk_log2 <= 2^30)
+    int nmax = nsteps;                      // warp-uniform bound
 #pragma unroll
-    for (int o = LPW; o < 32; o <<= 1) {
-        const uint64_t other = __shfl_xor_sync(FULLMASK, (unsigned long long)nmax, o);
-        nmax = other > nmax ? other : nmax;
-    }
+    for (int o = LPW; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(FULLMASK, nmax, o));
     // The flip position of step i (1-based; idle steps: any valid position, no writes).
-    const auto flip_pos = [&](uint64_t i) {
-        const int tz = aligned ? __ffs((unsigned)i) - 1 : __ffsll((long long)(g0 + i)) - 1;
+    const auto flip_pos = [&](int i) {
+        const int tz = aligned ? __ffs(i) - 1 : __ffsll((long long)(g0 + (uint64_t)i)) - 1;
         return i <= nsteps ? P.p + tz : P.p;
     };
     // The fused rule's [t = k-a] x_b term: x_b is read once, by the forward window at
     // t* = k-a, so it is zero in the array during the step (written flipped after it).  The
-    // zero of step i+1 is stored with step i's flips: one warp barrier per step.
+    // zero of step i+1 is stored with step i's flips: one store and two warp barriers per step.
     int a = flip_pos(1);
     if (nsteps >= 1 && sl == 2 && a != k) ((a & 1) ? X1 : X0)[P.xoff + ((L - 1 - a) >> 1)] = 0;
     __syncwarp();
-    for (uint64_t s0 = 0; s0 < nmax; s0 += LPW) {
-        const int nb = (int)(nsteps > s0 ? (nsteps - s0 < LPW ? nsteps - s0 : LPW) : 0);
-        const int nbw = (int)(nmax - s0 < LPW ? nmax - s0 : LPW);
+    // store lanes: 0 writes -x_a at a, 1 writes -x_b at b (not at the centre), 2 the next zero
+    const int st_lane = sl < 3 ? sl : 3;
+    for (int s0 = 0; s0 < nmax; s0 += LPW) {
+        const int nb = min(max(nsteps - s0, 0), LPW);
+        const int nbw = min(nmax - s0, LPW);
         int mine = 0;  // E after step s0 + sl
         for (int s = 0; s < nbw; ++s) {  // (rolled: small code, no instruction-cache misses)
             const bool live = s < nb;
-            const uint64_t i = s0 + s + 1;
+            const int i = s0 + s + 1;
             const int ah = a >> 1;
             int8_t* Xa = ((a & 1) ? X1 : X0) + P.xoff;
             const uint32_t* Xaw = (a & 1) ? X1w : X0w;
@@ -208,20 +207,22 @@ __device__ void enum_chunk(const EnumLaunch& P, int8_t* X0, int8_t* X1, uint64_t
             }
             const int tot = seg_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
             if (sl == s) mine = tot;
-            // stores: lane 0 x_a -> -x_a, lane 1 x_b -> -x_b, lane 2 the next step's x_b -> 0
             const int an = flip_pos(i + 1);
-            const bool st = sl == 0 ? live : (sl == 1 ? live && !cen : (sl == 2 && i < nsteps && an != k));
-            int8_t* dst = sl == 2 ? ((an & 1) ? X1 : X0) + P.xoff + ((L - 1 - an) >> 1)
-                                  : Xa + (sl == 0 ? ah : (L - 1 - a) >> 1);
-            const int8_t val = (int8_t)(sl == 0 ? -xa : (sl == 1 ? -xb : 0));
+            // (selects, not branches: every lane computes its store)
+            const int pa = st_lane == 2 ? an : a;
+            const int pos = st_lane == 0 ? ah : (L - 1 - pa) >> 1;
+            const int val = st_lane == 0 ? -xa : (st_lane == 1 ? -xb : 0);
+            const bool st = (st_lane == 0 && live) | (st_lane == 1 && live && !cen) |
+                            (st_lane == 2 && i < nsteps && an != k);
+            int8_t* dst = ((pa & 1) ? X1 : X0) + P.xoff + pos;
             __syncwarp();
-            if (st) *dst = val;
+            if (st) *dst = (int8_t)val;
             __syncwarp();
             a = an;
         }
         const bool vstep = sl < nb;
         const int e_mine = mine;
-        const uint64_t g_mine = g0 + 1 + s0 + sl;
+        const uint64_t g_mine = g0 + (uint64_t)(1 + s0 + sl);
         const int e_last = __shfl_sync(FULLMASK, e_mine, nb > 0 ? nb - 1 : 0, LPW);
         if (nb > 0) energy = e_last;
         if (vstep && e_mine < best_e) {
@@ -365,16 +366,25 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
     P.m = m;
     P.nj = (P.k + 127) / 128;
     P.nwx = (kp1 + 3) / 4;
-    // window reads reach SW+1 words past any position on both sides, SW = the lanes' lag
-    // words (up to S + 32: lanes past the lag range read zeros instead of branching); the
-    // correlation prologue reads up to nwx + S + 1 words
     const int S = (P.k + 3) / 4;
     P.S = S;
-    P.xoff = 4 * (S + 32) + 16;
-    P.xwords = ((P.xoff + 4 * P.nwx + 4 * (S + 32) + 32) / 4 + 3) & ~3;
+    // 4 lanes per chunk (eight chunks per warp share the per-step bookkeeping -- ctz, window
+    // addresses, the segment sum, the flip stores) up to 32 lag words, else 16 / 32;
+    // LABS_ENUM_LPW=4|8|16|32 forces a width (A/B timing)
+    const char* lenv = std::getenv("LABS_ENUM_LPW");
+    const int lwant = lenv ? std::atoi(lenv) : 0;
+    int lpw = S <= 32 ? 4 : (S <= 64 ? 16 : 32);
+    if (lwant == 32 || (lwant == 16 && S <= 64) || ((lwant == 8 || lwant == 4) && S <= 32)) lpw = lwant;
+    const int nj = (S + lpw - 1) / lpw;
+    // window reads reach SW+1 words past any position on both sides, SW = lpw x nj >= S the
+    // lanes' lag words (lanes past the lag range read zeros instead of branching); the
+    // correlation prologue reads up to nwx + SW + 1 words
+    const int SW = lpw * nj;
+    P.xoff = 4 * (SW + 2) + 16;
+    P.xwords = ((P.xoff + 4 * P.nwx + 4 * (SW + 2) + 32) / 4 + 3) & ~3;
     P.warp_words = 2 * P.xwords;
     const uint64_t range = g_end - g_begin;
-    int cl = chunk_log2 > 0 ? chunk_log2 : 12;
+    int cl = chunk_log2 > 0 ? std::min(chunk_log2, 30) : 12;  // (32-bit step counters)
     while (cl > 5 && (range >> cl) < 148ull * 32) --cl;  // enough chunks to fill the GPU
     P.chunk_log2 = cl;
     P.nchunks = (range + (1ull << cl) - 1) >> cl;
@@ -420,21 +430,11 @@ int enumerate_class_gpu(int32_t L, int32_t p, int32_t cls, int32_t m, int64_t e_
         P.chunk_next = cnt.p + 1;
         P.chunk_best = best.p;
         cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), stream);
-        // 8 or 16 lanes per chunk (four or two chunks per warp) while a lane owns <= 4 lag
-        // words; LABS_ENUM_LPW=8|16|32 forces a width (A/B timing)
-        const char* lenv = std::getenv("LABS_ENUM_LPW");
-        const int lwant = lenv ? std::atoi(lenv) : 0;
-        // (4 lanes: eight chunks per warp share the per-step bookkeeping -- ctz, window
-        // addresses, the segment sum, the flip stores -- which costs as much as the lag work)
-        int lpw = P.S <= 32 ? 4 : (P.S <= 64 ? 16 : 32);
-        if (lwant == 32 || (lwant == 16 && P.S <= 64) || ((lwant == 8 || lwant == 4) && P.S <= 32))
-            lpw = lwant;
         const int segs = 32 / lpw;
         const size_t smem = static_cast<size_t>(4) * segs * P.warp_words * 4;
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const uint64_t want = (P.nchunks + 4 * segs - 1) / (4 * segs);
-        const int nj = (P.S + lpw - 1) / lpw;
         cudaEventRecord(e0, stream);
         if (lpw == 4) {
             switch (nj) {
