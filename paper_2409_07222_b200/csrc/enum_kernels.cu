@@ -32,7 +32,8 @@ namespace labs_b200 {
 
 #define FULLMASK 0xffffffffu
 #ifndef LABS_ENUM_MINB
-#define LABS_ENUM_MINB 6  // resident 128-thread blocks per SM the 4-lane variants target (<= 85 registers)
+#define LABS_ENUM_MINB 7  // resident 128-thread blocks per SM the 4-lane variants target (72 registers;
+                          // 6 blocks at 80: 2.95e10, 8 at 64: 2.97e10, 7: 3.11e10 Gray steps/s)
 #endif
 
 struct EnumLaunch {
