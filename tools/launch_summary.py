@@ -24,7 +24,12 @@ print("serialised times: compare shares, not absolutes.\n")
 print("| kernel | launches | total ms | share |\n|---|---|---|---|")
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"| {k.split('(')[0]} | {n} | {t:.3f} | {100 * t / tot:.1f}% |")
-walk = sum(t for k, (n, t) in agg.items() if "saw_walk" in k and (", 0>" in k or ", false>" in k))
+def counting(k):  # the COUNT template argument (second of K1t's, last of K1's) is set
+    args = [a.strip() for a in k.split("<", 1)[1].split(">", 1)[0].split(",")]
+    return (args[1] if "mma" in k else args[-1]) in ("1", "true")
+
+
+walk = sum(t for k, (n, t) in agg.items() if "saw_walk" in k and not counting(k))
 seed = sum(t for k, (n, t) in agg.items() if "seed" in k)
 print(f"\nPer timed step the walk kernel is {100 * walk / (walk + seed):.2f}% of the device time "
       "(seed kernel the rest; the `<..., 1>` launch is the untimed delta-counting pass).")
