@@ -1,6 +1,7 @@
 // refine_b200.cpp -- Step 2 (refine, pq.cpp:114-176) scored through the GPU
 // neighbourhood kernel K5 (labs_pq_score), linked in place of the reference's CPU refine
-// (integration/Makefile compiles pq.cpp with `refine` / `refine_with_operators` renamed).
+// (integration/Makefile weakens the `refine` symbol of the reference's pq.o, so this
+// definition wins the link and the reference's refine_with_operators, pq.cpp:203-228, calls it).
 //
 // The frontier is the reference's own SearchFrontier (pq.hpp:37-70, pq.cpp:33-49) and its
 // operations run in exactly the reference order -- pop the pivot, then for i = 0..L-1:
@@ -101,33 +102,6 @@ RefineResult refine(const Candidate& start, const PqConfig& config) {
     }
     res.queue_exhausted = frontier.empty();
     return res;
-}
-
-// refine_with_operators (pq.cpp:203-228): the same alternation of refine and the six end
-// operators, restated so that it calls the GPU-scored refine above.
-std::map<int, Candidate> refine_with_operators(const Candidate& start, const PqConfig& config,
-                                               const std::set<int>& target_lengths) {
-    std::map<int, Candidate> best;
-    const auto improves = [&](const Candidate& c) {
-        if (!target_lengths.count(c.seq.length())) return false;
-        const auto it = best.find(c.seq.length());
-        return it == best.end() || c.energy < it->second.energy;
-    };
-    std::vector<Candidate> seeds{start};
-    std::unordered_set<std::uint64_t> seen_seeds{start.hash()};
-    while (!seeds.empty()) {
-        std::vector<Candidate> next;
-        for (const auto& seed : seeds) {
-            RefineResult r = refine(seed, config);
-            if (improves(r.best)) best.insert_or_assign(r.best.seq.length(), r.best);
-            if (r.best.seq.length() < 3) continue;
-            for (auto& derived : apply_length_operators(r.best.seq))
-                if (improves(derived) && seen_seeds.insert(derived.hash()).second)
-                    next.push_back(std::move(derived));
-        }
-        seeds = std::move(next);
-    }
-    return best;
 }
 
 }  // namespace labsearch
