@@ -245,12 +245,12 @@ def gpu_parity(labs, ref, walkers):
                         "its run_walk + DedupSink in --threads 1 order (oracle/_ref)"}
 
 
-def enum_c2(labs, peak, m=32):
+def enum_c2(labs, peak, m=36):
     """BASELINE config 2: K4 Gray enumeration of restriction class 0
-    at L=201, p=12, over the lowest m free half positions (the rest +1), sieve F >= 5.0.
-    Roofline: the FMA pipe (IDP4A + IMAD share it, 64 lanes/clk/SM): per Gray step every
-    even lag takes two IDP4A (its dc) and one IMAD (dc (2C + dc)), i.e. 3 FMA-pipe
-    lane-ops per lag, (L-1)/2 lags."""
+    at L=201, p=12, over the lowest m = 36 free half positions (the rest +1; 2^36 Gray
+    steps, ~2 s), sieve F >= 5.0.  Roofline: the FMA pipe (IDP4A + IMAD share it, 64
+    lanes/clk/SM): per Gray step every even lag takes two IDP4A (its dc) and one IMAD (its
+    C^2), i.e. 3 FMA-pipe lane-ops per lag, (L-1)/2 lags."""
     L2, p2, cls, e_l = 201, 12, 0, 4040
     labs.enumerate_class(L2, p2, cls, 20, e_l, collect=False)  # warm-up
     hits, st = labs.enumerate_class(L2, p2, cls, m, e_l, collect=False)
