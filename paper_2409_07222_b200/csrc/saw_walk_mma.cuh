@@ -338,7 +338,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         flip0 = c == 0 ? w.X(0) + P.xoff : reinterpret_cast<int8_t*>(w.Xc(0, c)) + P.xoff - c - P.xcl;
         flip1 = c == 0 ? w.X(1) + P.xoff : reinterpret_cast<int8_t*>(w.Xc(1, c)) + P.xoff - c - P.xcl;
     }
-    const bool one_key = L <= 1001;
+    const bool one_key = NQ == 1 || L <= 1001;  // (NQ = 1: L < 573, compile-time true)
     const bool dbg = P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
     uint32_t T[R];
