@@ -215,7 +215,10 @@ __device__ __forceinline__ void t_update_groups(const WalkParams& P, const uint3
     }
 }
 
-template <int NQ, bool COUNT>
+// MODE: 0 = the plain walk (the timed path), 1 = checked (debug_check_energy, score_out /
+// corr_out allowed), 2 = counting (count_visited: every neighbour's Bloom lookup counted;
+// also checked).  The plain kernel carries no per-step test of the diagnostic options.
+template <int NQ, int MODE>
 __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64_t* fm0,
                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
                              int* score_out, int* corr_out) {
@@ -339,7 +342,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         flip1 = c == 0 ? w.X(1) + P.xoff : reinterpret_cast<int8_t*>(w.Xc(1, c)) + P.xoff - c - P.xcl;
     }
     const bool one_key = NQ == 1 || L <= 1001;  // (NQ = 1: L < 573, compile-time true)
-    const bool dbg = P.debug_check != 0;
+    constexpr bool COUNT = MODE == 2;
+    constexpr bool CHK = MODE != 0;
+    const bool dbg = CHK && P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
     uint32_t T[R];
     int xs[R];
@@ -399,7 +404,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     long long evals_part = 0;
     int exhausted = 0;
     uint32_t skip = inval;
-    const int t_i32 = score_out ? 1 : (int)P.t_i;
+    const int t_i32 = (CHK && score_out) ? 1 : (int)P.t_i;
     bool active = valid;
 
     for (int it = 0;; ++it) {
@@ -431,7 +436,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             const int gv = acc[m / 8][(m >> 2) & 1][m & 3];
             delta[m] = (int)(T[m] + (uint32_t)xs[m] * (uint32_t)gv);
         }
-        if (score_out) {
+        if (CHK && score_out) {
             if (valid)
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
@@ -720,7 +725,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 
 // FMS: the flip-mask table fm has a shared copy per block (P.fm_words > 0, when that costs
 // no resident block) -- a compile-time choice, so its reads are shared loads, not generic ones
-template <int NQ, bool COUNT, bool FMS>
+template <int NQ, int MODE, bool FMS>
 __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     const uint64_t* fm = P.fm;
@@ -747,7 +752,7 @@ __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma
     int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp;
     while (walk < P.nwalks) {
         if (*(volatile int*)&P.ctl[1]) break;  // cancelled by the host (pool stopped)
-        run_walk_mma<NQ, COUNT>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, true, score_out, corr_out);
+        run_walk_mma<NQ, MODE>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, true, score_out, corr_out);
         unsigned long long nx = 0;
         if (lane == 0) nx = atomicAdd(P.walk_next, 1ull);
         walk = nwarps + (int64_t)__shfl_sync(FULLMASK, nx, 0);
@@ -758,8 +763,10 @@ template <int NQ>
 cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
                             int* score_out, int* corr_out, bool count) {
     const bool fms = P.fm_words > 0;
-    auto kfn = count ? (fms ? saw_walk_mma_kernel<NQ, true, true> : saw_walk_mma_kernel<NQ, true, false>)
-                     : (fms ? saw_walk_mma_kernel<NQ, false, true> : saw_walk_mma_kernel<NQ, false, false>);
+    const int mode = count ? 2 : ((P.debug_check || score_out || corr_out) ? 1 : 0);
+    auto kfn = fms ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
+    if (mode == 1) kfn = fms ? saw_walk_mma_kernel<NQ, 1, true> : saw_walk_mma_kernel<NQ, 1, false>;
+    if (mode == 2) kfn = fms ? saw_walk_mma_kernel<NQ, 2, true> : saw_walk_mma_kernel<NQ, 2, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kfn<<<grid, P.warps_per_block * 32, smem, st>>>(P, score_out, corr_out);
@@ -769,7 +776,7 @@ cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStre
 template <int NQ>
 int blocks_per_sm_mma(const WalkParams& P, size_t smem) {
     int n = 0;
-    auto kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, false, true> : saw_walk_mma_kernel<NQ, false, false>;
+    auto kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kfn, P.warps_per_block * 32, smem) != cudaSuccess)
         return 0;
