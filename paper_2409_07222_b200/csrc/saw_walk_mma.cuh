@@ -169,10 +169,14 @@ __device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int
     }
 }
 
-template <int NQ>
+template <int NQ, int NKS = 0>
 __device__ __forceinline__ void g_mma_any(const uint32_t* __restrict__ Kw, int nks, int kidx0, int xb,
                                           const uint32_t* __restrict__ xc0,
                                           const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
+    if (NKS > 0) {  // (a kernel specialised for this k-step count)
+        g_mma_fixed<NQ, (NKS > 0 ? NKS : 2)>(Kw, kidx0, xb, xc0, xc1, acc);
+        return;
+    }
     switch (nks) {  // (warp-uniform)
         case 8: g_mma_fixed<NQ, 8>(Kw, kidx0, xb, xc0, xc1, acc); break;
         case 10: g_mma_fixed<NQ, 10>(Kw, kidx0, xb, xc0, xc1, acc); break;
@@ -218,7 +222,8 @@ __device__ __forceinline__ void t_update_groups(const WalkParams& P, const uint3
 // MODE: 0 = the plain walk (the timed path), 1 = checked (debug_check_energy, score_out /
 // corr_out allowed), 2 = counting (count_visited: every neighbour's Bloom lookup counted;
 // also checked).  The plain kernel carries no per-step test of the diagnostic options.
-template <int NQ, int MODE>
+// NKS > 0: the k-step count is compile-time (plain kernels of the common lengths).
+template <int NQ, int MODE, int NKS>
 __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64_t* fm0,
                              const uint64_t* fm1, const uint64_t* fmf, int64_t walk, bool valid,
                              int* score_out, int* corr_out) {
@@ -419,7 +424,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 #pragma unroll
                 for (int i = 0; i < 4; ++i) acc[j][p2][i] = 0;
         if (wide) {  // G = 256 G_high + G_low
-            g_mma_any<NQ>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
+            g_mma_any<NQ, NKS>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
 #pragma unroll
             for (int j = 0; j < NQ; ++j)
 #pragma unroll
@@ -428,7 +433,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                     for (int i = 0; i < 4; ++i) acc[j][p2][i] *= 256;
             ++wide_iters;
         }
-        g_mma_any<NQ>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
+        g_mma_any<NQ, NKS>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
         // ---- exact deltas / keys: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
@@ -725,7 +730,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 
 // FMS: the flip-mask table fm has a shared copy per block (P.fm_words > 0, when that costs
 // no resident block) -- a compile-time choice, so its reads are shared loads, not generic ones
-template <int NQ, int MODE, bool FMS>
+template <int NQ, int MODE, bool FMS, int NKS = 0>
 __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma_kernel(WalkParams P, int* score_out, int* corr_out) {
     extern __shared__ uint4 smem_u4[];
     const uint64_t* fm = P.fm;
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma
     int64_t walk = (int64_t)blockIdx.x * P.warps_per_block + warp;
     while (walk < P.nwalks) {
         if (*(volatile int*)&P.ctl[1]) break;  // cancelled by the host (pool stopped)
-        run_walk_mma<NQ, MODE>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, true, score_out, corr_out);
+        run_walk_mma<NQ, MODE, NKS>(P, w, fm, fm + P.kp1, fm + 2 * P.kp1, walk, true, score_out, corr_out);
         unsigned long long nx = 0;
         if (lane == 0) nx = atomicAdd(P.walk_next, 1ull);
         walk = nwarps + (int64_t)__shfl_sync(FULLMASK, nx, 0);
@@ -765,6 +770,10 @@ cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStre
     const bool fms = P.fm_words > 0;
     const int mode = count ? 2 : ((P.debug_check || score_out || corr_out) ? 1 : 0);
     auto kfn = fms ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
+    if (NQ == 1 && mode == 0 && P.nks == 8)
+        kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
+    if (NQ == 1 && mode == 0 && P.nks == 10)
+        kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
     if (mode == 1) kfn = fms ? saw_walk_mma_kernel<NQ, 1, true> : saw_walk_mma_kernel<NQ, 1, false>;
     if (mode == 2) kfn = fms ? saw_walk_mma_kernel<NQ, 2, true> : saw_walk_mma_kernel<NQ, 2, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -777,6 +786,10 @@ template <int NQ>
 int blocks_per_sm_mma(const WalkParams& P, size_t smem) {
     int n = 0;
     auto kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
+    if (NQ == 1 && P.nks == 8)
+        kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
+    if (NQ == 1 && P.nks == 10)
+        kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kfn, P.warps_per_block * 32, smem) != cudaSuccess)
         return 0;
