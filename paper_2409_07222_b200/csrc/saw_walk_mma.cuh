@@ -770,10 +770,12 @@ cudaError_t launch_walk_mma(const WalkParams& P, int grid, size_t smem, cudaStre
     const bool fms = P.fm_words > 0;
     const int mode = count ? 2 : ((P.debug_check || score_out || corr_out) ? 1 : 0);
     auto kfn = fms ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
-    if (NQ == 1 && mode == 0 && P.nks == 8)
-        kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
-    if (NQ == 1 && mode == 0 && P.nks == 10)
-        kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
+    if constexpr (NQ == 1) {
+        if (mode == 0 && P.nks == 8)
+            kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
+        if (mode == 0 && P.nks == 10)
+            kfn = fms ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
+    }
     if (mode == 1) kfn = fms ? saw_walk_mma_kernel<NQ, 1, true> : saw_walk_mma_kernel<NQ, 1, false>;
     if (mode == 2) kfn = fms ? saw_walk_mma_kernel<NQ, 2, true> : saw_walk_mma_kernel<NQ, 2, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -786,10 +788,12 @@ template <int NQ>
 int blocks_per_sm_mma(const WalkParams& P, size_t smem) {
     int n = 0;
     auto kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true> : saw_walk_mma_kernel<NQ, 0, false>;
-    if (NQ == 1 && P.nks == 8)
-        kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
-    if (NQ == 1 && P.nks == 10)
-        kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
+    if constexpr (NQ == 1) {
+        if (P.nks == 8)
+            kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 8> : saw_walk_mma_kernel<NQ, 0, false, 8>;
+        if (P.nks == 10)
+            kfn = P.fm_words > 0 ? saw_walk_mma_kernel<NQ, 0, true, 10> : saw_walk_mma_kernel<NQ, 0, false, 10>;
+    }
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kfn, P.warps_per_block * 32, smem) != cudaSuccess)
         return 0;
