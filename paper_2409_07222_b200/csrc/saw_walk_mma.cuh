@@ -502,12 +502,12 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 ma = __reduce_min_sync(FULLMASK, mine);
                 mine_won = mine == ma;
             }
-            bool bit = true;
-            if (sl < P.bloom_k) {
-                const uint32_t idx = bloom_index(h1 ^ fm0[ma], h2 ^ fm1[ma], sl, P.bloom_mu, P.bloom_bits);
-                bit = (w.bloom[idx >> 5] >> (idx & 31)) & 1;
-                ins_idx = idx;
-            }
+            // (every lane computes its index -- no divergent branch; lanes past the k hashes
+            // read word 0, a broadcast, and count as set)
+            const bool hl = sl < P.bloom_k;
+            const uint32_t idx = bloom_index(h1 ^ fm0[ma], h2 ^ fm1[ma], sl, P.bloom_mu, P.bloom_bits);
+            const bool bit = !hl || ((w.bloom[hl ? idx >> 5 : 0] >> (idx & 31)) & 1);
+            ins_idx = idx;
             if (COUNT) {
                 dstar = md;
                 astar = ma;
