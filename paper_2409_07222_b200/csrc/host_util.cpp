@@ -206,7 +206,7 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.koff = koff;
     wp.kwords = round_up((koff + std::max(4 * wp.nwx, 4 * wp.S) + 16) / 4, 4);
     wp.hw = (wp.kp1 + 31) / 32;
-    if (bloom_bits >= (1ull << 32)) return "saw: Bloom filter exceeds 2^32 bits";
+    if (bloom_bits >= (1ull << 31)) return "saw: Bloom filter exceeds 2^31 bits";
     if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";
     wp.bloom_bits = static_cast<uint32_t>(bloom_bits);
     wp.bloom_k = bloom_k;
@@ -289,7 +289,7 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
     wp.koff = koff;
     wp.kwords = round_up((koff + std::max(32 * wp.nks + 16, 4 * wp.S + 16)) / 4, 4);
     wp.hw = (wp.kp1 + 31) / 32;
-    if (bloom_bits >= (1ull << 32)) return "saw: Bloom filter exceeds 2^32 bits";
+    if (bloom_bits >= (1ull << 31)) return "saw: Bloom filter exceeds 2^31 bits";
     if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";
     wp.bloom_bits = static_cast<uint32_t>(bloom_bits);
     wp.bloom_k = bloom_k;

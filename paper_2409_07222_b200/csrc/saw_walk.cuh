@@ -47,8 +47,9 @@ __device__ __forceinline__ uint32_t bloom_index(uint64_t h1, uint64_t h2, uint32
                                                 uint32_t m) {
     const uint64_t x = h1 + (uint64_t)i * h2;
     const uint64_t q = __umul64hi(x, mu);
-    const uint64_t r = x - q * (uint64_t)m;
-    return (uint32_t)(r >= m ? r - m : r);
+    // x - q m lies in [0, 2m) and m < 2^31 (make_walk_params): its low 32 bits are exact
+    const uint32_t r = (uint32_t)x - (uint32_t)q * m;
+    return r >= m ? r - m : r;
 }
 
 __device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int lane_mask) {
