@@ -170,6 +170,9 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
                                          uint64_t bloom_bits, int bloom_k, WalkParams& wp,
                                          int lpw_force) {
     wp = WalkParams{};
+    // (the (delta, hp) key fits 32 bits up to L = 1001; longer pools have >= 200 free half
+    // positions and run K1t)
+    if (L > 1001) return "saw: the IDP4A walk kernel covers L <= 1001 (K1t runs longer lengths)";
     wp.L = L;
     wp.k = (L - 1) / 2;
     wp.kp1 = wp.k + 1;

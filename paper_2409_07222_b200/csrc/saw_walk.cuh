@@ -415,8 +415,11 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     //     T'(a) = 512 T(a) + 2^31 + a,   xs' = 512 xs,
     // so that one IMAD, T' - xs' G, yields the key itself (wrapping mod 2^32 exactly like
     // the unsigned key).  Longer lengths keep the plain delta (sc = 1).
-    const bool one_key = L <= 1001;
-    const bool dbg = P.debug_check != 0;
+    // K1 runs L <= 1001 only (make_walk_params_impl): (delta, hp) always fit one key.  The
+    // diagnostic options (debug_check_energy, score_out) run in the COUNT kernels only, so the
+    // plain kernel has no per-step test of them.
+    constexpr bool one_key = true;
+    const bool dbg = COUNT && P.debug_check != 0;
     const int sc = one_key ? 512 : 1;
     uint32_t T[R];  // (unsigned: the key form wraps mod 2^32; meaningless for a > k, masked)
     int xs[R];  // NEGATED, key-scaled: -512 * 8 x_a (-512 * 4 x_k), so a key is one IMAD
@@ -480,7 +483,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
     for (int m = 0; m < R; ++m)
         if (a0 + 8 * m > k) inval |= 1u << m;
     uint32_t skip = inval;
-    const int64_t t_i = score_out ? 1 : P.t_i;
+    const int64_t t_i = (COUNT && score_out) ? 1 : P.t_i;
     bool active = valid;  // this segment's walk is still running
 
     const int t_i32 = (int)t_i;  // T_i < 2^28 (make_walk_params: Bloom bits < 2^32)
@@ -509,7 +512,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 #pragma unroll
         for (int m = 0; m < R; ++m)  // the key if one_key
             delta[m] = (int)(T[m] + (uint32_t)xs[m] * (uint32_t)acc[m]);
-        if (score_out) {
+        if (COUNT && score_out) {
             if (valid)
 #pragma unroll
                 for (int m = 0; m < R; ++m)
@@ -815,7 +818,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
         st[kWsBest] = best;
         st[kWsInitial] = e0;
         st[kWsExhausted] = exhausted;
-        st[kWsDeltaEvals] = COUNT ? evals_part : -1;
+        st[kWsDeltaEvals] = (COUNT && P.count_visited) ? evals_part : -1;
         st[kWsVisitedProbes] = probes;
         st[kWsWideIters] = wide_iters;
         st[kWsDiverged] = diverged;
@@ -884,7 +887,9 @@ __global__ void __launch_bounds__(128, (MinBlocks<R, LPW>::value))
 template <int R, int LPW>
 cudaError_t launch_walk_fixed(const WalkParams& P, int grid, size_t smem, cudaStream_t st,
                               int* score_out, int* corr_out, bool count) {
-    auto kfn = count ? saw_walk_kernel<R, LPW, true> : saw_walk_kernel<R, LPW, false>;
+    // (the COUNT kernel also serves the diagnostic options: the plain one never tests them)
+    const bool chk = count || P.debug_check || score_out || corr_out;
+    auto kfn = chk ? saw_walk_kernel<R, LPW, true> : saw_walk_kernel<R, LPW, false>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
