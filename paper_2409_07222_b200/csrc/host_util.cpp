@@ -279,6 +279,8 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
     wp.kdelta = ((3 - b0 - 7) % 4 + 4) % 4;       // (koff - D) == 0 mod 4, koff == 3 mod 4
     const int D = b0 + 7 + wp.kdelta;
     wp.nks = round_up((wp.kp1 + 7 + wp.kdelta + 31) / 32, 2);  // (even: g_mma's unroll)
+    if (wp.nq == 1 && wp.nks == 8 && (wp.S + 31) / 32 != 2)  // (the NKS = 8 kernels assume it)
+        return "saw: K1t geometry (8 k-steps with other than two lag words per lane)";
     // X: front reads down to -(k + 8) (T update, C update), B reads from -10; back reads up to
     // k/2 + 4S + 12 (C update), 4 (nwx + S + 3) (correlation init), 32 nks + 16 (B) and
     // 1.5 k + 4 (T update)

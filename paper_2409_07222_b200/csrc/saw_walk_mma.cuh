@@ -230,11 +230,12 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     constexpr int LPW = 32;
     constexpr int R = 8 * NQ;
     // lag words a lane owns: S = ceil(k/4) <= (2 b0 + 256 NQ + 3) / 4 with b0 <= 15
-    constexpr int NJ = (256 * NQ + 64 + 127) / 128 < 4 ? (256 * NQ + 64 + 127) / 128 : 4;
+    // (NKS = 8 implies 183 <= k+1 <= 249, 46 <= S <= 62: exactly two lag words per lane)
+    constexpr int NJ = NKS == 8 ? 2 : ((256 * NQ + 64 + 127) / 128 < 4 ? (256 * NQ + 64 + 127) / 128 : 4);
     const Seg<LPW> sg(threadIdx.x & 31);
     const int L = P.L, k = P.k, kp1 = P.kp1, S = P.S;
     const int sl = sg.sl;
-    const int nj = (S + LPW - 1) / LPW;
+    const int nj = NKS == 8 ? 2 : (S + LPW - 1) / LPW;
 
     // ---- load the initial half, build parity arrays + their byte-shifted copies ----
     const uint32_t* src = P.halves + (valid ? walk : 0) * P.hw;
