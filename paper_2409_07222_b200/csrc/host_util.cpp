@@ -281,18 +281,21 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
     wp.nks = round_up((wp.kp1 + 7 + wp.kdelta + 31) / 32, 2);  // (even: g_mma's unroll)
     if (wp.nq == 1 && wp.nks == 8 && (wp.S + 31) / 32 != 2)  // (the NKS = 8 kernels assume it)
         return "saw: K1t geometry (8 k-steps with other than two lag words per lane)";
-    // X: front reads down to -(k + 8) (T update, C update), B reads from -10; back reads up to
-    // k/2 + 4S + 12 (C update), 4 (nwx + S + 3) (correlation init), 32 nks + 16 (B) and
-    // 1.5 k + 4 (T update)
-    wp.xoff = 4 * round_up(std::max(wp.S + 2, (wp.k + 12) / 4 + 1), 2);
-    const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3),
+    // SW = 32 ceil(S/32): the lag words the lanes cover -- lanes past S update and store
+    // zeros (their windows read the zero padding) instead of branching.
+    // X: front reads down to -(4 SW + 8) (C update) and -(k + 8) (T update), B reads from -10;
+    // back reads up to k/2 + 4 SW + 12 (C update), 4 (nwx + S + 3) (correlation init),
+    // 32 nks + 16 (B) and 1.5 k + 4 (T update)
+    const int SW = 32 * ((wp.S + 31) / 32);
+    wp.xoff = 4 * round_up(std::max(SW + 2, (wp.k + 12) / 4 + 1), 2);
+    const int xhi = std::max({wp.k / 2 + 4 * SW + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3),
                               32 * wp.nks + 24, wp.k + wp.k / 2 + 8});
     wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
-    // K: A reads d from -(128 nq + D + 4) to 32 nks - D + 4; lag-word stores |d| <= 4S + 4
-    int koff = std::max(128 * wp.nq + D + 16, 4 * wp.S + 12);
+    // K: A reads d from -(128 nq + D + 4) to 32 nks - D + 4; lag-word stores |d| <= 4 SW + 4
+    int koff = std::max(128 * wp.nq + D + 16, 4 * SW + 12);
     while (koff % 4 != 3) ++koff;
     wp.koff = koff;
-    wp.kwords = round_up((koff + std::max(32 * wp.nks + 16, 4 * wp.S + 16)) / 4, 4);
+    wp.kwords = round_up((koff + std::max(32 * wp.nks + 16, 4 * SW + 16)) / 4, 4);
     wp.hw = (wp.kp1 + 31) / 32;
     if (bloom_bits >= (1ull << 31)) return "saw: Bloom filter exceeds 2^31 bits";
     if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";

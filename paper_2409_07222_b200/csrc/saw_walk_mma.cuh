@@ -630,7 +630,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
-                if (jj < nj && s < S) {
+                if (jj < nj) {  // (lanes past S: zero windows, C stays 0 -- no divergence)
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
                     LABS_BC(P, awF + s, 0, P.xwords - 1);
@@ -649,7 +649,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
             const int s = sl + LPW * jj;
             const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
-            if (jj < nj && s < S) store_k_word(ws, P, s, C[jj], cprev, wide_next);
+            if (jj < nj) store_k_word(ws, P, s, C[jj], cprev, wide_next);  // (zeros past S)
         }
         wide = wide_next;
         __syncwarp();
