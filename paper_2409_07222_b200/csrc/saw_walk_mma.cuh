@@ -557,11 +557,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         h1 ^= fm0[as];
         h2 ^= fm1[as];
         hf ^= fmf[as];
-        {  // Bloom insert by lanes 0..k_hash-1: a predicated shared reduction, not a branch
-            const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&w.bloom[ins_idx >> 5]);
-            asm volatile("{\n .reg .pred p;\n setp.lt.s32 p, %2, %3;\n @p red.shared.or.b32 [%0], %1;\n}"
-                         :: "r"(ba), "r"(1u << (ins_idx & 31)), "r"(sl), "r"(P.bloom_k) : "memory");
-        }
+        // Bloom insert by lanes 0..k_hash-1; the other lanes OR 0 into their (valid) word --
+        // no divergent branch around the atomic
+        atomicOr(&w.bloom[ins_idx >> 5], sl < P.bloom_k ? 1u << (ins_idx & 31) : 0u);
         energy += dstar;
         best = min(best, energy);
         // (1) zero x_a and x_b in the primary array (the T and C updates read the fused
@@ -569,7 +567,11 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         __syncwarp();
         // (lane 0 x_a*, lane 1 x_b*, the others byte -1 of the zero front padding: one store
         //  instruction, no branch)
-        Xa[sl == 0 ? ah : (sl == 1 ? (bstar >> 1) : -1)] = 0;
+        {
+            int zi = sl == 1 ? (bstar >> 1) : ah;
+            zi = sl >= 2 ? -1 : zi;
+            Xa[zi] = 0;
+        }
         __syncwarp();
         // (2) T updates from the zeroed pre-step sequence (K1's rules), four neighbours a = A + e
         //     (e = 0..3) per group at once.  Byte e of three windows holds f_a = x_{a*+2(k-a)},
