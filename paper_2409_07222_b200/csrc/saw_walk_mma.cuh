@@ -521,13 +521,17 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 astar = ma;
                 break;
             }
-            if (mine_won) {  // drop the visited neighbour, recompute this lane's minimum
+            if (one_key) {  // drop the visited neighbour from the winner's slots; every lane
+                            // recomputes its minimum (unchanged but for the winner: no branch)
+                const int d = ma - A0;
+                const int mm = (d >> 8) * 8 + (d & 1) * 4 + (((d & 255) >> 7) << 1) + ((d >> 1) & 1);
+                skip |= mine_won ? 1u << (mm & 31) : 0u;
+                bkey = lane_min_key<R>(delta, skip);
+            } else if (mine_won) {
                 const int d = ma - A0;
                 const int mm = (d >> 8) * 8 + (d & 1) * 4 + (((d & 255) >> 7) << 1) + ((d >> 1) & 1);
                 skip |= 1u << mm;
-                if (one_key) {
-                    bkey = lane_min_key<R>(delta, skip);
-                } else {
+                {
                     bd = INT_BIG;
                     bm = 0;
 #pragma unroll
@@ -619,7 +623,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 const uint32_t vx = (uint32_t)(8 * sc8 * xa * (int)Xa[(2 * aex - as) >> 1]);
 #pragma unroll
                 for (int m = 0; m < R; ++m)
-                    if (m == mx) T[m] += vx;
+                    T[m] += m == mx ? vx : 0u;  // (a select, not a divergent branch)
             }
         }
         // (3) even-lag C update, lanes over lag words: dc_t = mul (x_{a+2t} + x_{a-2t})
