@@ -312,8 +312,9 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
     wp.xcl = wp.xoff - 16;
     wp.xcw = 8 * wp.nks + 12;
     wp.off_xc = wp.off_x1 + wp.xwords;
-    wp.off_kl = wp.off_xc + 6 * wp.xcw;
-    wp.off_kh = wp.off_kl + wp.kwords;
+    wp.kpl = (wp.nq == 1 && wp.nks == 8) ? 1 : 0;
+    wp.off_kl = wp.off_xc + 6 * wp.xcw;             // KL, or KP (pair layout: 2 kwords + 32)
+    wp.off_kh = wp.off_kl + (wp.kpl ? 2 * wp.kwords + 32 : wp.kwords);
     wp.off_half = wp.off_kh + wp.kwords;
     wp.off_dc = wp.off_half;
     wp.off_bloom = wp.off_half + round_up(wp.hw, 4);

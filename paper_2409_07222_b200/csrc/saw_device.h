@@ -48,6 +48,9 @@ struct WalkParams {
     int32_t kdelta;                // K1t: D = p/2 + 7 + kdelta aligns the kernel words
     int32_t off_xc;                // K1t: three byte-shifted copies per parity array
     int32_t xcl, xcw;              // K1t: copy c word i = parity-array bytes xcl + 4i + c ..+3
+    int32_t kpl;                   // K1t: low kernel bytes in the A-fragment pair layout (KP)
+                                   //   -- one q-tile at 8 k-steps, where the extra words cost no
+                                   //   resident block; else plain (KL)
     int64_t nwalks;                // walks in this launch
     int64_t rec_cap;               // record ring slots (a power of two)
     // inputs (device pointers)

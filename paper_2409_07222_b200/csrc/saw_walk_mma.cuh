@@ -64,8 +64,9 @@ __device__ __forceinline__ void mma_s8(int (&d)[4], const uint32_t (&a)[4], uint
 struct MmaSmem {
     uint32_t* base;
     int off_x1, off_xc, xcw;
-    uint32_t* KL;        // correlation kernel, low / high bytes (byte koff + d = C_{2|d|})
-    uint32_t* KH;
+    uint32_t* KP;        // low kernel bytes: plain (KL, byte koff + d = low byte of C_{2|d|}) or,
+                         // with P.kpl, in A-fragment pairs KP[2i] = KL[i], KP[2i+1] = KL[i-16]
+    uint32_t* KH;        // high bytes, plain (byte koff + d = high byte of C_{2|d|})
     uint32_t* C16;       // (initialisation only, inside the Bloom words)
     int* KQ;
     uint32_t* half;
@@ -169,6 +170,54 @@ __device__ __forceinline__ void g_mma_fixed(const uint32_t* __restrict__ Kw, int
     }
 }
 
+// G from the pair layout KP: the A fragment of k-step s is two 8-byte loads, {a0, a1} =
+// KP[2i], KP[2i + 1] and {a2, a3} at i + 4 (i = kidx0 - 32 j + 8 s), straight into the
+// MMA's register quad (no register moves).  NKS = 0: runtime nks.
+template <int NQ, int NKS>
+__device__ __forceinline__ void g_mma_kp(const uint32_t* __restrict__ KP, int nks, int kidx0, int xb,
+                                         const uint32_t* __restrict__ xc0,
+                                         const uint32_t* __restrict__ xc1, int (&acc)[NQ][2][4]) {
+    const uint2* kp2 = reinterpret_cast<const uint2*>(KP) + kidx0;
+    const int n = NKS > 0 ? NKS : nks;
+#pragma unroll(NKS > 0 ? NKS : 2)
+    for (int s = 0; s < n; ++s) {
+        const uint32_t b00 = xc0[xb + 8 * s], b01 = xc0[xb + 8 * s + 4];
+        const uint32_t b10 = xc1[xb + 8 * s], b11 = xc1[xb + 8 * s + 4];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+            const uint2 lo = kp2[8 * s - 32 * j], hi = kp2[8 * s - 32 * j + 4];
+            const uint32_t a[4] = {lo.x, lo.y, hi.x, hi.y};
+            mma_s8(acc[j][0], a, b00, b01);
+            mma_s8(acc[j][1], a, b10, b11);
+        }
+    }
+}
+
+// Kernel words of lag word s (see store_c_word): the low bytes plain or into both places of
+// the pair layout (KPL: compile-time 1 / 0, or -1 = P.kpl), the high bytes (wide walks) plain.
+template <int KPL>
+__device__ __forceinline__ void store_kp_word(const MmaSmem& w, const WalkParams& P, int s,
+                                              const int (&c)[4], int cprev, bool wide) {
+    const int fw = (P.koff + 1) / 4 + s;
+    const int bw = (P.koff - 3) / 4 - s;
+    const uint32_t lo = pack4(c[0], c[1], c[2], c[3]);
+    const uint32_t lob = prmt(lo, (uint32_t)cprev, 0x4012);  // (c2, c1, c0, cprev)
+    if (KPL == 1 || (KPL < 0 && P.kpl)) {
+        w.KP[2 * fw] = lo;
+        w.KP[2 * fw + 33] = lo;
+        w.KP[2 * bw] = lob;
+        w.KP[2 * bw + 33] = lob;
+    } else {
+        w.KP[fw] = lo;
+        w.KP[bw] = lob;
+    }
+    if (wide) {
+        const uint32_t hi = pack4(hi_byte(c[0]), hi_byte(c[1]), hi_byte(c[2]), hi_byte(c[3]));
+        w.KH[fw] = hi;
+        w.KH[bw] = prmt(hi, (uint32_t)hi_byte(cprev), 0x4012);
+    }
+}
+
 template <int NQ, int NKS = 0>
 __device__ __forceinline__ void g_mma_any(const uint32_t* __restrict__ Kw, int nks, int kidx0, int xb,
                                           const uint32_t* __restrict__ xc0,
@@ -254,7 +303,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         }
         w.Xw(par)[word] = v;
     }
-    for (int i = sl; i < 2 * P.kwords; i += LPW) w.KL[i] = 0;  // KL and KH are adjacent
+    for (int i = sl; i < P.off_kh - P.off_kl + P.kwords; i += LPW) w.KP[i] = 0;  // (KP, KH adjacent)
     __syncwarp();
     for (int wi = sl; wi < 6 * P.xcw; wi += LPW) {  // copies c = 1..3 of both parities
         const int par = wi / (3 * P.xcw);
@@ -270,8 +319,6 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
     ws.X1 = w.X(1);
     ws.X0w = w.Xw(0);
     ws.X1w = w.Xw(1);
-    ws.KL = w.KL;
-    ws.KH = w.KH;
     ws.C16 = w.C16;
     ws.KQ = w.KQ;
     ws.half = w.half;
@@ -300,7 +347,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
         const int s = sl + LPW * jj;
         const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
         if (jj < nj && s < S) {
-            store_c_word(ws, P, s, C[jj], cprev, wide);
+            w.C16[2 * s] = prmt((uint32_t)C[jj][0], (uint32_t)C[jj][1], 0x5410);
+            w.C16[2 * s + 1] = prmt((uint32_t)C[jj][2], (uint32_t)C[jj][3], 0x5410);
+            store_kp_word<-1>(w, P, s, C[jj], cprev, wide);
             if (corr_out && valid)
                 for (int b = 0; b < 4; ++b)
                     if (4 * s + 1 + b <= k) corr_out[walk * k + 4 * s + b] = C[jj][b];
@@ -434,7 +483,9 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                     for (int i = 0; i < 4; ++i) acc[j][p2][i] *= 256;
             ++wide_iters;
         }
-        g_mma_any<NQ, NKS>(w.KL, P.nks, kidx0, xb, xc0, xc1, acc);
+        if (NKS == 8) g_mma_kp<NQ, 8>(w.KP, P.nks, kidx0, xb, xc0, xc1, acc);
+        else if (NKS > 0 || !P.kpl) g_mma_any<NQ, NKS>(w.KP, P.nks, kidx0, xb, xc0, xc1, acc);
+        else g_mma_kp<NQ, 0>(w.KP, P.nks, kidx0, xb, xc0, xc1, acc);
         // ---- exact deltas / keys: dE(a) = T(a) - xs(a) G(a) ----
         int delta[R];
 #pragma unroll
@@ -660,7 +711,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
             const int s = sl + LPW * jj;
             const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
-            if (jj < nj) store_k_word(ws, P, s, C[jj], cprev, wide_next);  // (zeros past S)
+            if (jj < nj) store_kp_word<NKS == 8 ? 1 : (NKS > 0 ? 0 : -1)>(w, P, s, C[jj], cprev, wide_next);  // (zeros past S)
         }
         wide = wide_next;
         __syncwarp();
@@ -759,7 +810,7 @@ __global__ void __launch_bounds__(128, NQ == 1 ? LABS_MMA_MINB : 3) saw_walk_mma
     w.off_x1 = P.off_x1;
     w.off_xc = P.off_xc;
     w.xcw = P.xcw;
-    w.KL = base + P.off_kl;
+    w.KP = base + P.off_kl;
     w.KH = base + P.off_kh;
     w.C16 = base + P.off_c16;
     w.KQ = reinterpret_cast<int*>(base + P.off_kq);
