@@ -402,33 +402,41 @@ def main():
         # roofline of the dominant kernel (the walk kernel: K1t at L=451): algorithmic int8 MACs
         # per launch / its CUDA-event duration.  The MAC work (the sliding dot products G) runs
         # on the int8 tensor cores (mma.sync) in K1t and on IDP4A in K1; both peaks are
-        # measured in this run.  `frac` keeps r01's basis (the CUDA-core IDP4A int8 MAC peak);
-        # `tensor` is the same work against the mma.sync int8 peak.  DESIGN.md §4: the step is
-        # bound by instruction issue of the per-step bookkeeping, not by either MAC pipe.
+        # measured in this run.  The step is bound by instruction issue of the per-step
+        # bookkeeping, not by either MAC pipe: for K1t the headline `frac` is the
+        # issue fraction (warp-instructions per walk iteration from the committed ncu capture x
+        # iterations/s over 4 SMSPs x SMs x clock); `idp4a` keeps r01's basis (the CUDA-core
+        # int8 MAC peak) and `tensor` is the same work against the mma.sync int8 peak.
         alg_ops = (deltas_rank + iters_rank) * OPS_PER_DELTA
         achieved = alg_ops / (st.kernel_ms / 1e3) / 1e12
         peak_v = peak["dp4a"] * 8 / 1e12 if peak else None
         imma = labs.imma_peak() if rank == 0 else None
         kern = labs.derive(labs.SawConfig(**base)).get("kernel", None)
-        roof = {"bound": "int32", "achieved": achieved, "peak": peak_v, "unit": "Tops/s",
-                "frac": (achieved / peak_v) if peak_v else None, "traffic": ncu_traffic(st.walks),
-                "traffic_source": "profile constant: profiles/ncu_summary.json (ncu --set full "
-                                  "capture of the walk kernel, DRAM bytes per walk x walks)",
-                "peak_source": "measured in this run (labs_int32_peak): IDP4A lane-instr/s x 8 "
-                               "int ops (4 int8 MACs), the CUDA-core int8 MAC peak (r01 basis)",
-                "tensor": {"peak": imma * 2 / 1e12 if imma else None, "unit": "Tops/s",
-                           "frac": achieved / (imma * 2 / 1e12) if imma else None,
-                           "peak_source": "measured in this run (labs_imma_peak): "
-                                          "mma.sync.m16n8k32.s8 int8 MACs/s x 2 ops"},
-                "walk_kernel": {0: "K1 (IDP4A G)", 1: "K1t (mma.sync int8 G)"}.get(kern, kern),
-                "issue": issue_roofline(iters_rank / (st.kernel_ms / 1e3), "ncu_summary.json",
-                                        "warp_instructions_per_walk_iteration", peak),
-                "int32_peak_detail": peak,
-                "alg_ops_per_launch": alg_ops,
-                "alg_unit": f"(reference-equivalent delta evals + applies) x (L+1) ops: one "
-                            f"delta = inner product of (L+1)/2 = {(L + 1) // 2} int8 MACs",
-                "kernel_ms_per_launch": st.kernel_ms,
-                "ref_equiv_tops": deltas_all * REF_OPS_PER_DELTA / step_s / 1e12}
+        issue = issue_roofline(iters_rank / (st.kernel_ms / 1e3), "ncu_summary.json",
+                               "warp_instructions_per_walk_iteration", peak)
+        idp4a = {"bound": "int32", "achieved": achieved, "peak": peak_v, "unit": "Tops/s",
+                 "frac": (achieved / peak_v) if peak_v else None,
+                 "peak_source": "measured in this run (labs_int32_peak): IDP4A lane-instr/s x 8 "
+                                "int ops (4 int8 MACs), the CUDA-core int8 MAC peak (r01 basis; "
+                                "K1t runs G on the tensor pipe, so this can pass 1)"}
+        tensor = {"peak": imma * 2 / 1e12 if imma else None, "unit": "Tops/s",
+                  "frac": achieved / (imma * 2 / 1e12) if imma else None,
+                  "peak_source": "measured in this run (labs_imma_peak): "
+                                 "mma.sync.m16n8k32.s8 int8 MACs/s x 2 ops"}
+        if kern == 1 and issue:  # K1t: instruction issue binds
+            roof = dict(issue, idp4a=idp4a)
+        else:  # K1: the IDP4A (FMA) pipe and issue
+            roof = dict(idp4a, issue=issue)
+        roof.update({"tensor": tensor, "traffic": ncu_traffic(st.walks),
+                     "traffic_source": "profile constant: profiles/ncu_summary.json (ncu --set full "
+                                       "capture of the walk kernel, DRAM bytes per walk x walks)",
+                     "walk_kernel": {0: "K1 (IDP4A G)", 1: "K1t (mma.sync int8 G)"}.get(kern, kern),
+                     "int32_peak_detail": peak,
+                     "alg_ops_per_launch": alg_ops,
+                     "alg_unit": f"(reference-equivalent delta evals + applies) x (L+1) ops: one "
+                                 f"delta = inner product of (L+1)/2 = {(L + 1) // 2} int8 MACs",
+                     "kernel_ms_per_launch": st.kernel_ms,
+                     "ref_equiv_tops": deltas_all * REF_OPS_PER_DELTA / step_s / 1e12})
         cpu, parity = None, None
         if not args.no_cpu_baseline:
             try:
