@@ -389,10 +389,17 @@ private:
             Executor& e = *ex_[static_cast<size_t>(g)];
             Gen& f = feed_[static_cast<size_t>(g)];
             const auto& wl = dev_walkers_[static_cast<size_t>(g)];
-            const int64_t chunk = chunk_[static_cast<size_t>(g)];
+            const int64_t total = static_cast<int64_t>(wl.size()) * R;
+            const int64_t half_wave = std::max<int64_t>(1, runners_[static_cast<size_t>(g)]->resident / 2);
             while (e.pushed() - e.popped() < kQueueDepth && f.k < wl.size()) {
                 Job job;
                 if (f.pre) job.pool_off = f.off;
+                // the last jobs shrink (half the remainder, down to half a wave): the host replay
+                // of the final job is all that follows the last kernel
+                const int64_t left = total - f.off;
+                const int64_t chunk = std::min(chunk_[static_cast<size_t>(g)],
+                                               left <= 2 * chunk_[static_cast<size_t>(g)]
+                                                   ? std::max(half_wave, (left + 1) / 2) : left);
                 while (job.nwalks < chunk && f.k < wl.size()) {
                     const int64_t take = std::min(R - f.r, chunk - job.nwalks);
                     job.segs.push_back(seg(wl[f.k], f.r, f.r + take));
