@@ -354,6 +354,7 @@ private:
     double wall_ms_per_walk_ = 0;    // consume wall time per walk of the latest batch
     int64_t last_batch_ = 1;         // walks of the latest coupled batch
     const bool timing_ = std::getenv("LABS_TIMING") != nullptr;
+    const bool shrink_ = !(std::getenv("LABS_TAIL_SHRINK") && std::string(std::getenv("LABS_TAIL_SHRINK")) == "0");
     // independent pools: per device, the next walk of its job list
     struct Gen {
         size_t k = 0;   // index into dev_walkers_[g]
@@ -398,7 +399,7 @@ private:
                 // of the final job is all that follows the last kernel
                 const int64_t left = total - f.off;
                 const int64_t chunk = std::min(chunk_[static_cast<size_t>(g)],
-                                               left <= 2 * chunk_[static_cast<size_t>(g)]
+                                               shrink_ && left <= 2 * chunk_[static_cast<size_t>(g)]
                                                    ? std::max(half_wave, (left + 1) / 2) : left);
                 while (job.nwalks < chunk && f.k < wl.size()) {
                     const int64_t take = std::min(R - f.r, chunk - job.nwalks);
