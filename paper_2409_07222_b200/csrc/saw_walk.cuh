@@ -648,16 +648,21 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             h1 ^= fm0[as];
             h2 ^= fm1[as];
             hf ^= fmf[as];
-            if (sl < P.bloom_k) atomicOr(&w.bloom[ins_idx >> 5], 1u << (ins_idx & 31));
-            if (LPW < 16 && sl + LPW < P.bloom_k) atomicOr(&w.bloom[ins_idx2 >> 5], 1u << (ins_idx2 & 31));
             energy += dstar;
             best = min(best, energy);
         }
+        // Bloom insert: lanes without a hash OR 0 into a valid word (no divergent branch)
+        atomicOr(&w.bloom[ins_idx >> 5], (step && sl < P.bloom_k) ? 1u << (ins_idx & 31) : 0u);
+        if (LPW < 16)
+            atomicOr(&w.bloom[ins_idx2 >> 5], (step && sl + LPW < P.bloom_k) ? 1u << (ins_idx2 & 31) : 0u);
         // (1) zero x_a and x_b: the Q pairs below and the C windows then read 0 there,
         //     which is exactly the fused rule's treatment of the flipped pair
         __syncwarp();
-        if (step && sl == 0) Xa[ah] = 0;
-        if (step && sl == 1) Xa[bstar >> 1] = 0;
+        {  // (lane 0 x_a*, lane 1 x_b*; the other lanes write byte -1 of the zero padding)
+            int zi = sl == 1 ? (bstar >> 1) : ah;
+            zi = (step && sl < 2) ? zi : -1;
+            Xa[zi] = 0;
+        }
         __syncwarp();
         // (2) T updates, all from the (zeroed) pre-step sequence, so their loads issue together
         //     with the C update's:
