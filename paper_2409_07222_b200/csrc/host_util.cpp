@@ -197,17 +197,20 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
     wp.S = std::max(1, (wp.k + 3) / 4);
     if (wp.S > 128) return "saw: length too large for the GPU path";
     wp.nwx = (wp.kp1 + 3) / 4;
-    // X arrays: backward reads down to index -(4S+4) (C update), forward reads up to
-    // k/2 + 4S + 8 (C update), 4*nwx (main loop) and 4*(nwx+S+2) (correlation init).
-    wp.xoff = 4 * round_up(wp.S + 2, 2);  // >= 4S+8, and the G loop's X words 8-byte aligned
-    const int xhi = std::max({wp.k / 2 + 4 * wp.S + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3)});
+    // SW = lpw ceil(S/lpw): the lag words the lanes cover -- lanes past S update and store
+    // zeros (their windows read the zero padding) instead of branching.
+    // X arrays: backward reads down to index -(4SW+4) (C update), forward reads up to
+    // k/2 + 4SW + 8 (C update), 4*nwx (main loop) and 4*(nwx+S+2) (correlation init).
+    const int SW = wp.lpw * ((wp.S + wp.lpw - 1) / wp.lpw);
+    wp.xoff = 4 * round_up(SW + 2, 2);  // >= 4SW+8, and the G loop's X words 8-byte aligned
+    const int xhi = std::max({wp.k / 2 + 4 * SW + 12, 4 * wp.nwx + 8, 4 * (wp.nwx + wp.S + 3)});
     wp.xwords = round_up((wp.xoff + xhi + 3) / 4, 4);
-    // kernel: main loop reads d in [-(p+lpw R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4S+4
+    // kernel: main loop reads d in [-(p+lpw R)/2 - 4R - 8, 4 nwx + 8]; lanes write |d| <= 4SW+4
     const int amax_h = (p + wp.lpw * wp.R) / 2 + 1;  // a0 + 8m < p + lpw R
-    int koff = std::max(amax_h + 4 * wp.R + 12, 4 * wp.S + 12);
+    int koff = std::max(amax_h + 4 * wp.R + 12, 4 * SW + 12);
     while (koff % 4 != 3) ++koff;
     wp.koff = koff;
-    wp.kwords = round_up((koff + std::max(4 * wp.nwx, 4 * wp.S) + 16) / 4, 4);
+    wp.kwords = round_up((koff + std::max(4 * wp.nwx, 4 * SW) + 16) / 4, 4);
     wp.hw = (wp.kp1 + 31) / 32;
     if (bloom_bits >= (1ull << 31)) return "saw: Bloom filter exceeds 2^31 bits";
     if (bloom_k > 32) return "saw: more than 32 Bloom hashes is not supported by the GPU path";

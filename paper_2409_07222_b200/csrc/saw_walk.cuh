@@ -717,7 +717,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 const int s = sl + LPW * jj;
-                if (jj < nj && s < S) {
+                if (jj < nj) {  // (lanes past S: zero windows, C stays 0 -- no divergence)
                     const uint32_t fw = prmt(Xaw[awF + s], Xaw[awF + s + 1], asF);
                     const uint32_t bw = prmt(Xaw[awB - s], Xaw[awB - s + 1], asB);
 #pragma unroll
@@ -735,7 +735,7 @@ __device__ void run_walk_seg(const WalkParams& P, const WarpSmem& w, const uint6
             const int wrap = __shfl_sync(FULLMASK, jj > 0 ? C[jj > 0 ? jj - 1 : 0][3] : 0, LPW - 1, LPW);
             const int s = sl + LPW * jj;
             const int cprev = s == 0 ? 0 : (sl == 0 ? wrap : up);
-            if (step && jj < nj && s < S) store_k_word(w, P, s, C[jj], cprev, wide_next);
+            if (step && jj < nj) store_k_word(w, P, s, C[jj], cprev, wide_next);  // (zeros past S)
         }
         if (step) wide = wide_next;
         __syncwarp();
