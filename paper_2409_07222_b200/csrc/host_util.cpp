@@ -170,7 +170,7 @@ static std::string make_walk_params_impl(int L, int p, int64_t t_i, int64_t e_l,
                                          uint64_t bloom_bits, int bloom_k, WalkParams& wp,
                                          int lpw_force) {
     wp = WalkParams{};
-    // (the (delta, hp) key fits 32 bits up to L = 1001; longer pools have >= 130 free half
+    // (the (delta, hp) key fits 32 bits up to L = 1001; longer pools have >= 150 free half
     // positions and run K1t)
     if (L > 1001) return "saw: the IDP4A walk kernel covers L <= 1001 (K1t runs longer lengths)";
     wp.L = L;
@@ -340,8 +340,8 @@ static std::string make_walk_params_mma(int L, int p, int64_t t_i, int64_t e_l,
 
 // Which walk kernel: K1t (tensor-core G) from kMmaMinFree free half positions on, K1
 // below (LABS_KERNEL=dp4a|mma forces one: A/B timing, tests).
-static constexpr int kMmaMinFree = 130;  // (same-box crossover: K1 wins at 128 free bits,
-                                         //  K1t at 133 -- tools/ab_kernels_by_length.sh)
+static constexpr int kMmaMinFree = 150;  // (same-box crossover: K1 wins at 143 free bits,
+                                         //  K1t at 153 -- tools/ab_kernels_by_length.sh)
 
 std::string make_walk_params(int L, int p, int64_t t_i, int64_t e_l, uint64_t bloom_bits,
                              int bloom_k, WalkParams& wp) {
