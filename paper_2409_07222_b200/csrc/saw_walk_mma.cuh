@@ -473,7 +473,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             for (int p2 = 0; p2 < 2; ++p2)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) acc[j][p2][i] = 0;
-        if (wide) {  // G = 256 G_high + G_low
+        if (__builtin_expect(wide, 0)) {  // G = 256 G_high + G_low (rare)
             g_mma_any<NQ, NKS>(w.KH, P.nks, kidx0, xb, xc0, xc1, acc);
 #pragma unroll
             for (int j = 0; j < NQ; ++j)
@@ -543,7 +543,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             bool mine_won;
             if (one_key) {
                 const uint32_t k_best = __reduce_min_sync(FULLMASK, bkey);
-                if (k_best == 0xffffffffu) break;  // every free neighbour visited
+                if (__builtin_expect(k_best == 0xffffffffu, 0)) break;  // every free neighbour visited
                 ma = (int)(k_best & 511u);
                 md = (int)(k_best >> 9) - (1 << 22);
                 mine_won = bkey == k_best;
@@ -594,7 +594,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
                 }
             }
         }
-        if (astar < 0) {
+        if (__builtin_expect(astar < 0, 0)) {
             exhausted = 1;
             active = false;
             break;
@@ -729,7 +729,7 @@ __device__ void run_walk_mma(const WalkParams& P, const MmaSmem& w, const uint64
             if (sg.sum(esp) != energy) ++diverged;
         }
         __syncwarp();
-        if (energy < P.e_l) {  // K2: one ring slot (warp-uniform: one walk per warp)
+        if (__builtin_expect(energy < P.e_l, 0)) {  // K2: one ring slot (warp-uniform: one walk per warp)
             ++emitted;
             unsigned long long slot = 0;
             if (sl == 0) slot = atomicAdd(P.rec_count, 1ull);
